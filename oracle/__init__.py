@@ -1,0 +1,184 @@
+"""CPU oracle for the discretised Stokes BIO apply (arXiv 1707.06551).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package; the product
+package paper_1707_06551_b200 never does.  The arithmetic lives in
+oracle/oracle.cpp (plain C++, fp64, -ffp-contract=off, Neumaier sums); this
+file only compiles it and marshals numpy arrays through ctypes.
+
+Functions follow SURVEY.md §8(c) O-1..O-7; each cites its PAPER.md passage in
+oracle.cpp.  Parity status per function is recorded in DESIGN.md §4.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_DP = ctypes.POINTER(ctypes.c_double)
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile oracle.cpp -> liboracle.so (g++ -O2 -ffp-contract=off -fopenmp)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+               "-shared", "-o", _LIB + ".tmp", _SRC]
+        subprocess.run(cmd, check=True)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        lib = ctypes.CDLL(_LIB)
+        i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        lib.oracle_gl_rule.argtypes = [i32, _DP, _DP]
+        lib.oracle_nodes.argtypes = [_DP, _DP, i64, i32, _DP, _DP, _DP]
+        lib.oracle_far.argtypes = [_DP, _DP, i64, i32, d, _DP, _DP, _I64P, i64, _DP]
+        lib.oracle_self.argtypes = [_DP, _DP, i64, i32, d, _DP, _DP, _I64P, i64, _DP]
+        lib.oracle_offsurface.argtypes = [_DP, _DP, i64, i32, d, _DP, _DP, _DP, i64, _DP, _DP]
+        lib.oracle_self_addthm.argtypes = [i32, d, d, _DP, _DP, _DP]
+        lib.oracle_ylm.argtypes = [i32, i32, d, d, _DP]
+        lib.oracle_ylm.restype = None
+        lib.oracle_vsh.argtypes = [i32, i32, d, d, _DP]
+        lib.oracle_vsh.restype = None
+        lib.oracle_eigen.argtypes = [i32, i32, _DP, _DP, _DP, _DP]
+        lib.oracle_eigen.restype = None
+        lib.oracle_num_threads.restype = i32
+        lib.oracle_set_num_threads.argtypes = [i32]
+        lib.oracle_set_num_threads.restype = None
+        _lib = lib
+    return _lib
+
+
+def _dp(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_DP)
+
+
+def _c(a, dtype=np.float64):
+    return None if a is None else np.ascontiguousarray(a, dtype=dtype)
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    _load().oracle_set_num_threads(int(n))
+
+
+def gl_rule(p: int):
+    """O-1: (t, lambda) of the (p+1)-point Gauss-Legendre rule, t ascending."""
+    t = np.empty(p + 1)
+    lam = np.empty(p + 1)
+    if _load().oracle_gl_rule(p, _dp(t), _dp(lam)) != 0:
+        raise ValueError("gl_rule: bad p")
+    return t, lam
+
+
+def nodes(centres, radii, p: int):
+    """O-2: x [N,3], outward normals [N,3], weights [N] in node order."""
+    centres = _c(centres)
+    radii = _c(radii)
+    ns = len(radii)
+    N = ns * (p + 1) * (2 * p + 2)
+    x = np.empty((N, 3))
+    n = np.empty((N, 3))
+    w = np.empty(N)
+    if _load().oracle_nodes(_dp(centres), _dp(radii), ns, p, _dp(x), _dp(n), _dp(w)) != 0:
+        raise ValueError("nodes: bad arguments")
+    return x, n, w
+
+
+def _subset(idx, N):
+    if idx is None:
+        idx = np.arange(N, dtype=np.int64)
+    return np.ascontiguousarray(idx, dtype=np.int64)
+
+
+def far(centres, radii, p, mu, f, q, subset=None):
+    """O-3: smooth-rule S[f] + D[q] over all other spheres at nodes `subset`."""
+    centres, radii, f, q = _c(centres), _c(radii), _c(f), _c(q)
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    idx = _subset(subset, N)
+    u = np.empty((len(idx), 3))
+    rc = _load().oracle_far(_dp(centres), _dp(radii), len(radii), p, mu, _dp(f), _dp(q),
+                            idx.ctypes.data_as(_I64P), len(idx), _dp(u))
+    if rc:
+        raise ValueError("far: bad arguments")
+    return u
+
+
+def self_term(centres, radii, p, mu, f, q, subset=None):
+    """O-4: spectral self term (a/mu) S_self[f] + D_pv,self[q] at nodes `subset`."""
+    centres, radii, f, q = _c(centres), _c(radii), _c(f), _c(q)
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    idx = _subset(subset, N)
+    u = np.empty((len(idx), 3))
+    rc = _load().oracle_self(_dp(centres), _dp(radii), len(radii), p, mu, _dp(f), _dp(q),
+                             idx.ctypes.data_as(_I64P), len(idx), _dp(u))
+    if rc:
+        raise ValueError("self_term: bad arguments")
+    return u
+
+
+def apply(centres, radii, p, mu, f, q, subset=None):
+    """O-5: u = far + self = S[f] + D_pv[q] at nodes `subset` (no 1/2 I)."""
+    return far(centres, radii, p, mu, f, q, subset) + self_term(centres, radii, p, mu, f, q, subset)
+
+
+def offsurface(centres, radii, p, mu, f, q, targets):
+    """O-6: velocity [M,3] and pressure [M] at arbitrary targets (all sources)."""
+    centres, radii, f, q, targets = _c(centres), _c(radii), _c(f), _c(q), _c(targets)
+    M = 0 if targets is None else targets.shape[0]
+    u = np.empty((M, 3))
+    pr = np.empty(M)
+    rc = _load().oracle_offsurface(_dp(centres), _dp(radii), len(radii), p, mu, _dp(f), _dp(q),
+                                   _dp(targets) if M else None, M, _dp(u), _dp(pr))
+    if rc:
+        raise ValueError("offsurface: bad arguments")
+    return u, pr
+
+
+def self_addthm(p, mu, a, f, q):
+    """O-7: one sphere's self operator via the addition theorem (all its nodes)."""
+    f, q = _c(f), _c(q)
+    ns = (p + 1) * (2 * p + 2)
+    u = np.empty((ns, 3))
+    if _load().oracle_self_addthm(p, mu, a, _dp(f), _dp(q), _dp(u)) != 0:
+        raise ValueError("self_addthm: bad arguments")
+    return u
+
+
+def ylm(n, m, theta, phi):
+    """Y_n^m (eq 2.1), dY/dtheta, (1/sin theta) dY/dphi as complex numbers."""
+    out = np.empty(6)
+    _load().oracle_ylm(n, m, theta, phi, _dp(out))
+    return complex(out[0], out[1]), complex(out[2], out[3]), complex(out[4], out[5])
+
+
+def vsh(n, m, theta, phi):
+    """Cartesian complex V, W, X (eqs 2.4-2.6) at (theta, phi), shape [3 (V,W,X), 3]."""
+    out = np.empty(18)
+    _load().oracle_vsh(n, m, theta, phi, _dp(out))
+    z = out[0::2] + 1j * out[1::2]
+    return z.reshape(3, 3)
+
+
+def eigen(n, ch):
+    """(lamS, lamD_ext, lamD_int, lamD_pv) for channel ch (0=V, 1=W, 2=X), unit sphere."""
+    v = [ctypes.c_double() for _ in range(4)]
+    _load().oracle_eigen(n, ch, *[ctypes.byref(x) for x in v])
+    return tuple(x.value for x in v)

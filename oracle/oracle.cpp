@@ -1,0 +1,501 @@
+// =============================================================================
+// oracle/oracle.cpp -- plain, slow, obviously-correct CPU oracle for the
+// discretised Stokes boundary-integral-operator apply of Corona & Veerapaneni,
+// arXiv 1707.06551.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs may load this library.  It
+// shares no code, header, table or constant generator with the CUDA path in
+// paper_1707_06551_b200/ and never calls it.
+//
+// Precision: IEEE fp64, compiled with -O2 -ffp-contract=off (no FMA
+// contraction, no fast-math); far-field and off-surface sums use Neumaier
+// compensated accumulation in ascending source order.
+//
+// Citations "P:n" are PAPER.md line numbers; "SURVEY" is /root/repo/SURVEY.md;
+// readings of garbled/ambiguous passages are listed in DESIGN.md §3.
+//
+// Steps:
+//   O-1 oracle_gl_rule      Gauss-Legendre rule, eq 4.2
+//   O-2 oracle_nodes        nodes/normals/weights, eqs 4.2, 4.4,
+//                           reading R4 (w = a^2 lambda_j 2pi/(2p+2))
+//   O-3 oracle_far          smooth Nystrom sum of S and D, eqs 2.19-2.21, 4.4
+//                           (P:121-132), stresslet sign reading R1,
+//                           own sphere excluded (reading R8)
+//   O-4 oracle_self         self term: discrete VSH projection (eqs 2.1, 2.3,
+//                           2.4-2.6), diagonal scale by the r->1
+//                           limits of eqs 3.6-3.11 (readings R2,R3),
+//                           inverse expansion (eq 2.12)
+//   O-6 oracle_offsurface   velocity + pressure at arbitrary targets (reading R12)
+//   O-7 oracle_self_addthm  the same self operator built from the addition
+//                           theorem, an internal cross-check
+//   helpers for pins: oracle_ylm, oracle_vsh, oracle_eigen
+// =============================================================================
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstdlib>
+#include <vector>
+#include <omp.h>
+
+typedef std::complex<double> cplx;
+static const double PI = 3.141592653589793238462643383279502884;
+
+// ---------------------------------------------------------------- utilities
+struct Neumaier {  // compensated summation (Neumaier's variant of Kahan)
+  double s = 0.0, c = 0.0;
+  void add(double v) {
+    double t = s + v;
+    if (std::fabs(s) >= std::fabs(v)) c += (s - t) + v;
+    else c += (v - t) + s;
+    s = t;
+  }
+  double get() const { return s + c; }
+};
+
+// Legendre polynomial P_n(x) and derivative via the three-term recurrence.
+static void legendre_pn(int n, double x, double* Pn, double* dPn) {
+  double p0 = 1.0, p1 = x;
+  if (n == 0) { *Pn = 1.0; *dPn = 0.0; return; }
+  for (int k = 2; k <= n; ++k) {
+    double pk = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+    p0 = p1; p1 = pk;
+  }
+  *Pn = p1;
+  *dPn = n * (x * p1 - p0) / (x * x - 1.0);
+}
+
+// ------------------------------------------------------------------ O-1
+// (p+1)-point Gauss-Legendre rule on [-1,1], nodes ascending (eq 4.2).
+extern "C" int oracle_gl_rule(int p, double* t, double* lam) {
+  if (p < 0 || !t || !lam) return 1;
+  const int n = p + 1;
+  for (int j = 0; j < n; ++j) {
+    double x = -std::cos(PI * (j + 0.75) / (n + 0.5));
+    double P, dP;
+    for (int it = 0; it < 100; ++it) {
+      legendre_pn(n, x, &P, &dP);
+      double dx = P / dP;
+      x -= dx;
+      if (std::fabs(dx) < 1e-15) break;
+    }
+    legendre_pn(n, x, &P, &dP);  // one extra step
+    x -= P / dP;
+    legendre_pn(n, x, &P, &dP);
+    t[j] = x;
+    lam[j] = 2.0 / ((1.0 - x * x) * dP * dP);
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ O-2
+// Node i = s*(p+1)(2p+2) + j*(2p+2) + k: n = (sin th_j cos ph_k,
+// sin th_j sin ph_k, t_j), x = c_s + a_s n, w = a_s^2 lambda_j 2pi/(2p+2).
+extern "C" int oracle_nodes(const double* centres, const double* radii, int64_t ns, int p,
+                            double* x, double* nrm, double* w) {
+  if (ns < 1 || p < 1 || !centres || !radii) return 1;
+  const int nphi = 2 * p + 2, nsn = (p + 1) * nphi;
+  std::vector<double> t(p + 1), lam(p + 1);
+  oracle_gl_rule(p, t.data(), lam.data());
+  for (int64_t s = 0; s < ns; ++s)
+    for (int j = 0; j <= p; ++j)
+      for (int k = 0; k < nphi; ++k) {
+        int64_t i = s * nsn + (int64_t)j * nphi + k;
+        double st = std::sqrt(1.0 - t[j] * t[j]);
+        double ph = 2.0 * PI * k / nphi;
+        double n3[3] = {st * std::cos(ph), st * std::sin(ph), t[j]};
+        for (int c = 0; c < 3; ++c) {
+          if (nrm) nrm[3 * i + c] = n3[c];
+          if (x) x[3 * i + c] = centres[3 * s + c] + radii[s] * n3[c];
+        }
+        if (w) w[i] = radii[s] * radii[s] * lam[j] * 2.0 * PI / nphi;
+      }
+  return 0;
+}
+
+struct Geometry {
+  int p, nphi, nsn;
+  int64_t ns, N;
+  std::vector<double> x, n, w;
+  Geometry(const double* c, const double* a, int64_t ns_, int p_) : p(p_), ns(ns_) {
+    nphi = 2 * p + 2;
+    nsn = (p + 1) * nphi;
+    N = ns * nsn;
+    x.resize(3 * N); n.resize(3 * N); w.resize(N);
+    oracle_nodes(c, a, ns, p, x.data(), n.data(), w.data());
+  }
+};
+
+// Smooth-rule contribution of source k at point xt (eqs 2.19-2.21 with 4.4):
+//   S: w_k (1/(8 pi mu)) (f/r + (rho.f) rho / r^3)            (eq 2.19)
+//   D: w_k (3/(4 pi)) (rho.n)(rho.q) rho / r^5                 (eq 2.20, R1)
+//   pressure (R12): w_k [ (1/(4pi)) (rho.f)/r^3
+//                         + (mu/(2pi)) (-(q.n)/r^3 + 3 (rho.q)(rho.n)/r^5) ]
+static inline void pair_terms(const double* xt, const double* y, const double* ny, double wk,
+                              const double* f, const double* q, double mu, double u[3],
+                              double* pr) {
+  double rho[3] = {xt[0] - y[0], xt[1] - y[1], xt[2] - y[2]};
+  double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
+  double r = std::sqrt(r2);
+  double r3 = r2 * r, r5 = r3 * r2;
+  u[0] = u[1] = u[2] = 0.0;
+  double pv = 0.0;
+  if (f) {
+    double rf = rho[0] * f[0] + rho[1] * f[1] + rho[2] * f[2];
+    double cS = wk / (8.0 * PI * mu);
+    for (int c = 0; c < 3; ++c) u[c] += cS * (f[c] / r + rf * rho[c] / r3);
+    pv += wk * rf / (4.0 * PI * r3);
+  }
+  if (q) {
+    double rn = rho[0] * ny[0] + rho[1] * ny[1] + rho[2] * ny[2];
+    double rq = rho[0] * q[0] + rho[1] * q[1] + rho[2] * q[2];
+    double qn = q[0] * ny[0] + q[1] * ny[1] + q[2] * ny[2];
+    double cD = 3.0 * wk / (4.0 * PI);
+    for (int c = 0; c < 3; ++c) u[c] += cD * rn * rq * rho[c] / r5;
+    pv += wk * mu / (2.0 * PI) * (-qn / r3 + 3.0 * rq * rn / r5);
+  }
+  if (pr) *pr = pv;
+}
+
+// ------------------------------------------------------------------ O-3
+// Far field at the subset of nodes tidx[0..nt): sum over every node of every
+// OTHER sphere (reading R8), ascending source index, Neumaier per component.
+extern "C" int oracle_far(const double* centres, const double* radii, int64_t ns, int p,
+                          double mu, const double* f, const double* q, const int64_t* tidx,
+                          int64_t nt, double* u) {
+  if (ns < 1 || p < 1 || !(mu > 0) || !u || !tidx) return 1;
+  Geometry G(centres, radii, ns, p);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t i = tidx[t];
+    const int64_t si = i / G.nsn;
+    Neumaier acc[3];
+    for (int64_t k = 0; k < G.N; ++k) {
+      if (k / G.nsn == si) continue;
+      double v[3];
+      pair_terms(&G.x[3 * i], &G.x[3 * k], &G.n[3 * k], G.w[k], f ? f + 3 * k : nullptr,
+                 q ? q + 3 * k : nullptr, mu, v, nullptr);
+      for (int c = 0; c < 3; ++c) acc[c].add(v[c]);
+    }
+    for (int c = 0; c < 3; ++c) u[3 * t + c] = acc[c].get();
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ O-6
+// Off-surface velocity and pressure: sum over ALL nodes (no exclusion).
+extern "C" int oracle_offsurface(const double* centres, const double* radii, int64_t ns, int p,
+                                 double mu, const double* f, const double* q,
+                                 const double* targets, int64_t m, double* u, double* pres) {
+  if (ns < 1 || p < 1 || !(mu > 0) || (m > 0 && (!targets || !u))) return 1;
+  Geometry G(centres, radii, ns, p);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < m; ++t) {
+    Neumaier acc[3], pacc;
+    for (int64_t k = 0; k < G.N; ++k) {
+      double v[3], pv;
+      pair_terms(&targets[3 * t], &G.x[3 * k], &G.n[3 * k], G.w[k], f ? f + 3 * k : nullptr,
+                 q ? q + 3 * k : nullptr, mu, v, &pv);
+      for (int c = 0; c < 3; ++c) acc[c].add(v[c]);
+      pacc.add(pv);
+    }
+    for (int c = 0; c < 3; ++c) u[3 * t + c] = acc[c].get();
+    if (pres) pres[t] = pacc.get();
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------- harmonics (eq 2.1)
+// Unnormalised associated Legendre P_n^m(x), m >= 0, WITHOUT the
+// Condon-Shortley phase (eq 2.1 writes P_n^{|m|} with no phase), and
+// d/dtheta P_n^m(cos theta) = (n cos th P_n^m - (n+m) P_{n-1}^m) / sin th.
+static void assoc_legendre(int n, int m, double x, double* P, double* dPdth) {
+  double s = std::sqrt(1.0 - x * x);
+  double pmm = 1.0;
+  for (int k = 1; k <= m; ++k) pmm *= (2.0 * k - 1.0) * s;  // (2m-1)!! s^m
+  double pprev = 0.0, pcur = pmm;                             // P_{m-1}^m = 0
+  for (int l = m + 1; l <= n; ++l) {
+    double pn = ((2.0 * l - 1.0) * x * pcur - (l + m - 1.0) * pprev) / (l - m);
+    pprev = pcur;
+    pcur = pn;
+  }
+  *P = pcur;  // P_n^m ; pprev = P_{n-1}^m (0 when n == m)
+  *dPdth = (n * x * pcur - (n + m) * pprev) / s;
+}
+
+static double ynm_norm(int n, int m) {  // sqrt((2n+1)/(4pi) (n-|m|)!/(n+|m|)!)
+  int am = std::abs(m);
+  double ratio = 1.0;
+  for (int k = n - am + 1; k <= n + am; ++k) ratio /= k;
+  return std::sqrt((2.0 * n + 1.0) / (4.0 * PI) * ratio);
+}
+
+// Y_n^m(theta,phi), dY/dtheta and (1/sin theta) dY/dphi (eq 2.1).
+static void ynm_all(int n, int m, double th, double ph, cplx* Y, cplx* dY, cplx* dYphi) {
+  int am = std::abs(m);
+  double P, dP;
+  assoc_legendre(n, am, std::cos(th), &P, &dP);
+  double N = ynm_norm(n, m);
+  cplx e = std::polar(1.0, m * ph);
+  *Y = N * P * e;
+  *dY = N * dP * e;
+  *dYphi = cplx(0.0, (double)m) * N * P * e / std::sin(th);
+}
+
+// Cartesian V, W, X (eqs 2.4-2.6) at (th, ph): out[0..2]=V, [3..5]=W, [6..8]=X.
+static void vsh_cart(int n, int m, double th, double ph, cplx out[9]) {
+  cplx Y, dY, dYp;
+  ynm_all(n, m, th, ph, &Y, &dY, &dYp);
+  double st = std::sin(th), ct = std::cos(th), sp = std::sin(ph), cp = std::cos(ph);
+  double er[3] = {st * cp, st * sp, ct}, et[3] = {ct * cp, ct * sp, -st}, ep[3] = {-sp, cp, 0.0};
+  for (int c = 0; c < 3; ++c) {
+    cplx grad = dY * et[c] + dYp * ep[c];               // surface gradient
+    out[c] = grad - (double)(n + 1) * Y * er[c];        // V  (2.4)
+    out[3 + c] = grad + (double)n * Y * er[c];          // W  (2.5)
+    out[6 + c] = dY * ep[c] - dYp * et[c];              // X = e_r x grad (2.6)
+  }
+}
+
+extern "C" void oracle_ylm(int n, int m, double th, double ph, double* out6) {
+  cplx Y, dY, dYp;
+  ynm_all(n, m, th, ph, &Y, &dY, &dYp);
+  out6[0] = Y.real(); out6[1] = Y.imag();
+  out6[2] = dY.real(); out6[3] = dY.imag();
+  out6[4] = dYp.real(); out6[5] = dYp.imag();
+}
+
+extern "C" void oracle_vsh(int n, int m, double th, double ph, double* out18) {
+  cplx z[9];
+  vsh_cart(n, m, th, ph, z);
+  for (int c = 0; c < 9; ++c) { out18[2 * c] = z[c].real(); out18[2 * c + 1] = z[c].imag(); }
+}
+
+// ------------------------------------------------------- eigenvalues (Thm 2)
+// Unit sphere, mu = 1.  Channel ch: 0=V, 1=W, 2=X.  The r->1 limits of the
+// exterior/interior branches of eqs 3.6-3.8 (S) and 3.9-3.11 (D);
+// at r = 1 the cross terms vanish.  S is continuous (reading R3); the on-surface
+// D is the principal value, the mean of the two limits (reading R2).
+extern "C" void oracle_eigen(int n, int ch, double* lamS, double* lamD_ext, double* lamD_int,
+                             double* lamD_pv) {
+  double a = 2.0 * n + 1.0;
+  double S = 0, De = 0, Di = 0;
+  if (ch == 0) {         // V_n
+    S = n / (a * (2.0 * n + 3.0));
+    De = (2.0 * n * n + 4.0 * n + 3.0) / (a * (2.0 * n + 3.0));
+    Di = -2.0 * n * (n + 2.0) / (a * (2.0 * n + 3.0));
+  } else if (ch == 1) {  // W_n
+    S = (n + 1.0) / (a * (2.0 * n - 1.0));
+    De = 2.0 * (n + 1.0) * (n - 1.0) / (a * (2.0 * n - 1.0));
+    Di = -(2.0 * n * n + 1.0) / (a * (2.0 * n - 1.0));
+  } else {               // X_n
+    S = 1.0 / a;
+    De = (n - 1.0) / a;
+    Di = -(n + 2.0) / a;
+  }
+  if (lamS) *lamS = S;
+  if (lamD_ext) *lamD_ext = De;
+  if (lamD_int) *lamD_int = Di;
+  if (lamD_pv) *lamD_pv = 0.5 * (De + Di);
+}
+
+// ||Z_n||^2 on the unit sphere: V (n+1)(2n+1), W n(2n+1), X n(n+1).
+static double vsh_norm2(int n, int ch) {
+  if (ch == 0) return (n + 1.0) * (2.0 * n + 1.0);
+  if (ch == 1) return n * (2.0 * n + 1.0);
+  return n * (n + 1.0);
+}
+
+// ------------------------------------------------------------------ O-4
+// Self term at the subset nodes tidx[0..nt):
+//   alpha^Z_nm[g] = (1/||Z_n||^2) sum_{k in sphere} w^_k g_k . conj Z_nm(k),
+//     w^_k = lambda_j 2pi/(2p+2), g in {(a/mu) f, q}            (eq 2.3 discretised)
+//   psi = lamS(n,Z) alpha[(a/mu) f] + lamD_pv(n,Z) alpha[q]      (Thm 2)
+//   u_i = Re sum_{n<=p, m, Z} psi Z_nm(i)                         (eq 2.12)
+extern "C" int oracle_self(const double* centres, const double* radii, int64_t ns, int p,
+                           double mu, const double* f, const double* q, const int64_t* tidx,
+                           int64_t nt, double* u) {
+  if (ns < 1 || p < 1 || !(mu > 0) || !u || !tidx) return 1;
+  (void)centres;
+  const int nphi = 2 * p + 2, nsn = (p + 1) * nphi;
+  std::vector<double> t(p + 1), lam(p + 1);
+  oracle_gl_rule(p, t.data(), lam.data());
+  // table of Z_nm at the unit-grid nodes: index ((k*(p+1)^2 + (n*n+n+m))*3 + ch)*3 + c
+  const int nlm = (p + 1) * (p + 1);
+  std::vector<cplx> Z((size_t)nsn * nlm * 9);
+  std::vector<double> what(nsn);
+  for (int j = 0; j <= p; ++j)
+    for (int k = 0; k < nphi; ++k) {
+      int kk = j * nphi + k;
+      what[kk] = lam[j] * 2.0 * PI / nphi;
+      double th = std::acos(t[j]), ph = 2.0 * PI * k / nphi;
+      for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m) {
+          cplx z[9];
+          vsh_cart(n, m, th, ph, z);
+          for (int c = 0; c < 9; ++c) Z[((size_t)kk * nlm + n * n + n + m) * 9 + c] = z[c];
+        }
+    }
+  // group targets by sphere
+  std::vector<int64_t> order(nt);
+  for (int64_t a = 0; a < nt; ++a) order[a] = a;
+  std::vector<int64_t> sph(nt);
+  for (int64_t a = 0; a < nt; ++a) sph[a] = tidx[a] / nsn;
+  std::vector<int64_t> uniq(sph);
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t ui = 0; ui < (int64_t)uniq.size(); ++ui) {
+    const int64_t s = uniq[ui];
+    const double aS = radii[s] / mu;
+    std::vector<cplx> psi((size_t)nlm * 3, cplx(0.0, 0.0));
+    for (int n = 0; n <= p; ++n)
+      for (int m = -n; m <= n; ++m)
+        for (int ch = 0; ch < 3; ++ch) {
+          if (n == 0 && ch > 0) continue;  // W_0 = X_0 = 0 (reading R7)
+          cplx af(0.0, 0.0), aq(0.0, 0.0);
+          for (int kk = 0; kk < nsn; ++kk) {
+            const cplx* z = &Z[((size_t)kk * nlm + n * n + n + m) * 9 + 3 * ch];
+            int64_t i = s * nsn + kk;
+            for (int c = 0; c < 3; ++c) {
+              if (f) af += what[kk] * aS * f[3 * i + c] * std::conj(z[c]);
+              if (q) aq += what[kk] * q[3 * i + c] * std::conj(z[c]);
+            }
+          }
+          double nn = vsh_norm2(n, ch);
+          double lS, lD;
+          oracle_eigen(n, ch, &lS, nullptr, nullptr, &lD);
+          psi[(size_t)(n * n + n + m) * 3 + ch] = lS * af / nn + lD * aq / nn;
+        }
+    for (int64_t a = 0; a < nt; ++a) {
+      if (sph[a] != s) continue;
+      int kk = (int)(tidx[a] - s * nsn);
+      cplx acc[3] = {0.0, 0.0, 0.0};
+      for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m)
+          for (int ch = 0; ch < 3; ++ch) {
+            if (n == 0 && ch > 0) continue;
+            cplx ps = psi[(size_t)(n * n + n + m) * 3 + ch];
+            const cplx* z = &Z[((size_t)kk * nlm + n * n + n + m) * 9 + 3 * ch];
+            for (int c = 0; c < 3; ++c) acc[c] += ps * z[c];
+          }
+      for (int c = 0; c < 3; ++c) u[3 * a + c] = acc[c].real();
+    }
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ O-7
+// The same discrete self operator on ONE sphere (all its nodes), built from
+// the addition theorem instead of explicit harmonics:
+//   sum_m Y(x) conj Y(y)          = c_n P_n(t),                 t = x.y
+//   sum_m gradY(x) conj Y(y)      = c_n P_n'(t) (y - t x)
+//   sum_m Y(x) conj gradY(y)      = c_n P_n'(t) (x - t y)
+//   sum_m gradY(x) (x) conj gradY(y) = c_n [P_n''(t)(y - t x)(x - t y)^T
+//                                        + P_n'(t)(I - x x^T)(I - y y^T)]
+// with c_n = (2n+1)/(4 pi), V = gradY - (n+1) Y x, W = gradY + n Y x,
+// X = x cross gradY.  u_i = sum_k w^_k sum_n sum_Z lam_Z(n)/||Z_n||^2 K_n^ZZ(x_i,x_k) g_k.
+extern "C" int oracle_self_addthm(int p, double mu, double a, const double* f, const double* q,
+                                  double* u) {
+  if (p < 1 || !(mu > 0) || !(a > 0) || !u) return 1;
+  const int nphi = 2 * p + 2, nsn = (p + 1) * nphi;
+  std::vector<double> t(p + 1), lam(p + 1);
+  oracle_gl_rule(p, t.data(), lam.data());
+  std::vector<double> X(3 * nsn), wh(nsn);
+  for (int j = 0; j <= p; ++j)
+    for (int k = 0; k < nphi; ++k) {
+      int kk = j * nphi + k;
+      double st = std::sqrt(1.0 - t[j] * t[j]), ph = 2.0 * PI * k / nphi;
+      X[3 * kk] = st * std::cos(ph);
+      X[3 * kk + 1] = st * std::sin(ph);
+      X[3 * kk + 2] = t[j];
+      wh[kk] = lam[j] * 2.0 * PI / nphi;
+    }
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int i = 0; i < nsn; ++i) {
+    const double* x = &X[3 * i];
+    double acc[3] = {0, 0, 0};
+    for (int k = 0; k < nsn; ++k) {
+      const double* y = &X[3 * k];
+      double tt = x[0] * y[0] + x[1] * y[1] + x[2] * y[2];
+      // P_n, P_n', P_n'' by upward recurrences valid at t = +-1
+      std::vector<double> P(p + 1), dP(p + 1), ddP(p + 1);
+      P[0] = 1; dP[0] = 0; ddP[0] = 0;
+      if (p >= 1) { P[1] = tt; dP[1] = 1; ddP[1] = 0; }
+      for (int n = 2; n <= p; ++n) {
+        P[n] = ((2.0 * n - 1.0) * tt * P[n - 1] - (n - 1.0) * P[n - 2]) / n;
+        dP[n] = dP[n - 2] + (2.0 * n - 1.0) * P[n - 1];
+        ddP[n] = ddP[n - 2] + (2.0 * n - 1.0) * dP[n - 1];
+      }
+      double ytx[3], xty[3];
+      for (int c = 0; c < 3; ++c) { ytx[c] = y[c] - tt * x[c]; xty[c] = x[c] - tt * y[c]; }
+      double Px[9], Py[9];  // I - x x^T, I - y y^T
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          Px[3 * r + c] = (r == c) - x[r] * x[c];
+          Py[3 * r + c] = (r == c) - y[r] * y[c];
+        }
+      double PxPy[9];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          double s = 0;
+          for (int l = 0; l < 3; ++l) s += Px[3 * r + l] * Py[3 * l + c];
+          PxPy[3 * r + c] = s;
+        }
+      double KS[9] = {0}, KD[9] = {0};
+      for (int n = 0; n <= p; ++n) {
+        double cn = (2.0 * n + 1.0) / (4.0 * PI);
+        double A0 = cn * P[n];
+        double A1[3], A1p[3], T[9];
+        for (int c = 0; c < 3; ++c) { A1[c] = cn * dP[n] * ytx[c]; A1p[c] = cn * dP[n] * xty[c]; }
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c)
+            T[3 * r + c] = cn * (ddP[n] * ytx[r] * xty[c] + dP[n] * PxPy[3 * r + c]);
+        double KV[9], KW[9], KX[9];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) {
+            KV[3 * r + c] = T[3 * r + c] - (n + 1.0) * A1[r] * y[c] - (n + 1.0) * x[r] * A1p[c] +
+                            (n + 1.0) * (n + 1.0) * A0 * x[r] * y[c];
+            KW[3 * r + c] = T[3 * r + c] + n * A1[r] * y[c] + n * x[r] * A1p[c] +
+                            (double)n * n * A0 * x[r] * y[c];
+          }
+        // KX = [x]_x T [y]_x^T ; [v]_x w = v cross w
+        double Cx[9] = {0, -x[2], x[1], x[2], 0, -x[0], -x[1], x[0], 0};
+        double Cy[9] = {0, -y[2], y[1], y[2], 0, -y[0], -y[1], y[0], 0};
+        double tmp[9];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) {
+            double s = 0;
+            for (int l = 0; l < 3; ++l) s += Cx[3 * r + l] * T[3 * l + c];
+            tmp[3 * r + c] = s;
+          }
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) {
+            double s = 0;
+            for (int l = 0; l < 3; ++l) s += tmp[3 * r + l] * Cy[3 * c + l];
+            KX[3 * r + c] = s;
+          }
+        double lS[3], lD[3];
+        for (int ch = 0; ch < 3; ++ch) oracle_eigen(n, ch, &lS[ch], nullptr, nullptr, &lD[ch]);
+        for (int e = 0; e < 9; ++e) {
+          KS[e] += lS[0] / vsh_norm2(n, 0) * KV[e];
+          KD[e] += lD[0] / vsh_norm2(n, 0) * KV[e];
+          if (n >= 1) {
+            KS[e] += lS[1] / vsh_norm2(n, 1) * KW[e] + lS[2] / vsh_norm2(n, 2) * KX[e];
+            KD[e] += lD[1] / vsh_norm2(n, 1) * KW[e] + lD[2] / vsh_norm2(n, 2) * KX[e];
+          }
+        }
+      }
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          if (f) acc[r] += wh[k] * KS[3 * r + c] * (a / mu) * f[3 * k + c];
+          if (q) acc[r] += wh[k] * KD[3 * r + c] * q[3 * k + c];
+        }
+    }
+    for (int c = 0; c < 3; ++c) u[3 * i + c] = acc[c];
+  }
+  return 0;
+}
+
+extern "C" int oracle_num_threads(void) { return omp_get_max_threads(); }
+extern "C" void oracle_set_num_threads(int n) { if (n > 0) omp_set_num_threads(n); }
