@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Stokes BIO apply (arXiv 1707.06551 hot path).
+
+One step = one pass of every row of SURVEY.md §8(a) over the workload:
+bie_apply_SLDL (pack + spectral self term + far-field SL+DL pair sum at every
+node) followed by bie_eval_offsurface (velocity + pressure at the off-surface
+targets).  Default workload: BASELINE.json configs[4] ("cfg5": 10,000 unit
+spheres, p = 6, 980,000 nodes, 1,000,000 off-surface targets), the largest
+configuration that exercises all rows; --config 4 times the 1.38M-node apply.
+
+Metric (BASELINE.json): fp64 pair-interactions/s.  A pair is one (target,
+source node) interaction of the fused SL+DL kernel: N (N - n_s) for the apply
+(own sphere excluded) plus M N off-surface.  Inputs are resident in HBM when
+the timed region starts; L2 (126 MB) is flushed between timed steps with a
+256 MB write.  `e2e` times the host-buffer C-ABI entry points (pinned host
+memory, H2D + D2H inside the timed region).
+
+Multi-GPU: replicas only: each rank runs the same workload on
+its own GPU, no data-path collective; value = total pairs / max-over-ranks time.
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on a
+bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_PAIR = 48      # 18 DFMA (x2) + 9 DMUL + 3 DADD
+FP64_OPS_PER_PAIR = 30   # FP64-pipe instructions per pair (apply)
+FP64_OPS_PER_PAIR_OFF = 32
+N_SM = 148
+FP64_LANES = 64          # FP64 FMA lanes per SM (B200)
+SM_MAX_MHZ = 1965.0
+
+
+def peak_fp64_tflops(mhz=SM_MAX_MHZ):
+    return N_SM * FP64_LANES * 2 * mhz * 1e6 / 1e12
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def workload(cfg):
+    from bie_inputs import make_config
+    d = make_config(cfg, with_targets=(cfg == 5))
+    return d
+
+
+def nsn_of(p):
+    return (p + 1) * (2 * p + 2)
+
+
+def pair_counts(d):
+    N = d["n_nodes"]
+    ns = nsn_of(d["p"])
+    apply_pairs = N * (N - ns)
+    M = 0 if d["targets"] is None else len(d["targets"])
+    return apply_pairs, M * N, M
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import torch
+    import paper_1707_06551_b200 as bie
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    d = workload(args.config)
+    from bie_inputs import rigid_field
+    p, mu = d["p"], d["mu"]
+    ctx = bie.bie_create(d["centres"], d["radii"], p, mu)
+    N = bie.bie_num_nodes(ctx)
+    f_np, q_np = d["f"], d["q"]
+    if d["rigid"] is not None:
+        x = torch.empty((N, 3), dtype=torch.float64, device=dev)
+        bie.bie_get_nodes(ctx, x)
+        q_np = rigid_field(*d["rigid"], x.cpu().numpy(), d["centres"], nsn_of(p))
+    if d["same_fq"]:
+        f_np = q_np
+    f = torch.from_numpy(np.ascontiguousarray(f_np)).to(dev)
+    q = torch.from_numpy(np.ascontiguousarray(q_np)).to(dev)
+    u = torch.empty((N, 3), dtype=torch.float64, device=dev)
+    has_off = d["targets"] is not None
+    if has_off:
+        tg = torch.from_numpy(d["targets"]).to(dev)
+        M = tg.shape[0]
+        uo = torch.empty((M, 3), dtype=torch.float64, device=dev)
+        po = torch.empty(M, dtype=torch.float64, device=dev)
+    apply_pairs, off_pairs, M = pair_counts(d)
+    step_pairs = apply_pairs + off_pairs
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        bie.bie_apply_SLDL(ctx, f, q, u, stream)
+        if has_off:
+            bie.bie_eval_offsurface(ctx, f, q, tg, uo, po, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    bie.bie_reset_profile(ctx)
+    bie.bie_set_profiling(ctx, True)
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    prof = bie.bie_get_profile(ctx)
+    bie.bie_set_profiling(ctx, False)
+    total_ms = float(sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * step_pairs * args.steps / (total_ms / 1e3)
+    launches = int(sum(v[1] for k, v in prof.items() if k != "copy"))
+
+    # dominant kernel: far-field pair sum of the apply (k_nbody)
+    nb_ms = prof["nbody"][0] / args.steps
+    nb_pairs_s = apply_pairs / (nb_ms / 1e3)
+    achieved = nb_pairs_s * FLOPS_PER_PAIR / 1e12
+    peak = peak_fp64_tflops()
+    roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "k_nbody<4,128,64,3,false> (far-field SL+DL, row a3)",
+                "peak_source": "derived: 148 SM x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (DESIGN.md §5)",
+                "fp64_pipe_frac": round(nb_pairs_s * FP64_OPS_PER_PAIR / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)}
+    if clk.get("sm_mhz"):
+        roofline["fp64_pipe_frac_at_measured_clock"] = round(
+            nb_pairs_s * FP64_OPS_PER_PAIR / (N_SM * FP64_LANES * clk["sm_mhz"] * 1e6), 4)
+    kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
+               for k, v in prof.items() if v[1]}
+    if has_off and prof["offsurface"][0] > 0:
+        off_ms = prof["offsurface"][0] / args.steps
+        kernels["offsurface"]["pairs_per_s"] = off_pairs / (off_ms / 1e3)
+        kernels["offsurface"]["fp64_pipe_frac"] = round(
+            off_pairs / (off_ms / 1e3) * FP64_OPS_PER_PAIR_OFF / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)
+    kernels["nbody"]["pairs_per_s"] = nb_pairs_s
+
+    # ---- e2e through the host-buffer entry points (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        fh = torch.from_numpy(np.ascontiguousarray(f_np)).pin_memory()
+        qh = torch.from_numpy(np.ascontiguousarray(q_np)).pin_memory()
+        uh = torch.empty((N, 3), dtype=torch.float64).pin_memory()
+        h2d = 2 * N * 3 * 8
+        d2h = N * 3 * 8
+        if has_off:
+            tgh = torch.from_numpy(d["targets"]).pin_memory()
+            uoh = torch.empty((M, 3), dtype=torch.float64).pin_memory()
+            poh = torch.empty(M, dtype=torch.float64).pin_memory()
+            h2d += 2 * N * 3 * 8 + M * 3 * 8
+            d2h += M * 4 * 8
+
+        def step_host():
+            bie.bie_apply_SLDL_host(ctx, fh, qh, uh, stream)
+            if has_off:
+                bie.bie_eval_offsurface_host(ctx, fh, qh, tgh, uoh, poh, stream)
+
+        step_host()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        et = []
+        for _ in range(args.e2e_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step_host()
+            e1.record(stream)
+            e1.synchronize()
+            et.append(e0.elapsed_time(e1))
+        tot = float(sum(et))
+        if world > 1:
+            t = torch.tensor([tot], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            tot = float(t.item())
+        e2e = {"value": world * step_pairs * args.e2e_steps / (tot / 1e3), "unit": "pair-interactions/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "ms_per_step": tot / args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(d, f_np, q_np, budget_s=args.cpu_seconds)
+
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    if rank != 0:
+        return
+    cfg_names = {4: "cfg4: 4096 unit spheres jittered lattice, p=12, D[q]+S[q]",
+                 5: "cfg5: 10000 unit spheres RSA side 60, p=6, apply + 1e6 off-surface targets"}
+    out = {
+        "metric": "fp64 pair-interactions/sec for SL+DL apply; % of B200 FP64 peak",
+        "value": value, "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE.json recipe, bie_inputs/)",
+        "config": {"workload": f"cfg{args.config}",
+                   "description": cfg_names.get(args.config, CONFIG_DESC(args.config)),
+                   "n_spheres": int(len(d["radii"])), "p": p, "n_nodes": int(N),
+                   "n_offsurface_targets": int(M), "apply_pairs": int(apply_pairs),
+                   "offsurface_pairs": int(off_pairs), "l2": "flushed (256 MB write) between timed steps",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clk,
+        "gpu_launches": launches,
+        "kernels": kernels,
+        "step_ms": [round(t, 3) for t in times],
+    }
+    print(json.dumps(out))
+
+
+def CONFIG_DESC(c):
+    from bie_inputs import CONFIGS
+    return CONFIGS.get(c, "")
+
+
+# ------------------------------------------------------------------ CPU oracle
+def cpu_baseline(d, f_np, q_np, budget_s=15.0, kind="oracle"):
+    """Time the oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+    oracle.build_oracle()
+    cores = oracle.num_threads()
+    N = d["n_nodes"]
+    ns = nsn_of(d["p"])
+    rng = np.random.default_rng(12345)
+    has_off = d["targets"] is not None
+    share = 0.5 if has_off else 1.0
+
+    def timed_apply(nt):
+        sub = np.sort(rng.choice(N, nt, replace=False))
+        t0 = time.perf_counter()
+        oracle.apply(d["centres"], d["radii"], d["p"], d["mu"], f_np, q_np, sub)
+        return time.perf_counter() - t0, nt * (N - ns)
+
+    def timed_off(nt):
+        idx = np.sort(rng.choice(len(d["targets"]), nt, replace=False))
+        t0 = time.perf_counter()
+        oracle.offsurface(d["centres"], d["radii"], d["p"], d["mu"], f_np, q_np, d["targets"][idx])
+        return time.perf_counter() - t0, nt * N
+
+    probe = max(8, 2 * cores)
+    t, _ = timed_apply(probe)
+    nt = int(min(N, max(probe, probe * share * budget_s / max(t, 1e-3))))
+    ta, pa = timed_apply(nt)
+    tot_t, tot_p, desc = ta, pa, f"{nt} random nodes of the apply (far + self)"
+    if has_off:
+        t, _ = timed_off(probe)
+        mo = int(min(len(d["targets"]), max(probe, probe * share * budget_s / max(t, 1e-3))))
+        to, po_ = timed_off(mo)
+        tot_t += to
+        tot_p += po_
+        desc += f" + {mo} random off-surface targets"
+    return {"value": tot_p / tot_t, "unit": "pair-interactions/s", "cores": cores, "kind": kind,
+            "sample": desc + f" of cfg, {tot_t:.1f} s wall"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    d = workload(args.config)
+    f_np, q_np = d["f"], d["q"]
+    if d["rigid"] is not None:
+        import oracle
+        x, _, _ = oracle.nodes(d["centres"], d["radii"], d["p"])
+        from bie_inputs import rigid_field
+        q_np = rigid_field(*d["rigid"], x, d["centres"], nsn_of(d["p"]))
+    if d["same_fq"]:
+        f_np = q_np
+    per_step = max(2.0, args.cpu_seconds / max(args.steps, 1))
+    for _ in range(args.warmup):
+        cpu_baseline(d, f_np, q_np, budget_s=0.2)
+    vals, secs = [], 0.0
+    res = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = cpu_baseline(d, f_np, q_np, budget_s=per_step)
+        secs += time.perf_counter() - t0
+        vals.append(res["value"])
+    v = float(np.median(vals))
+    res["value"] = v
+    out = {"impl": "reference", "metric": "fp64 pair-interactions/sec for SL+DL apply; % of B200 FP64 peak",
+           "value": v, "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded BASELINE.json recipe, bie_inputs/)",
+           "config": {"workload": f"cfg{args.config}", "note": "CPU oracle on a bounded sample per step"},
+           "cpu_baseline": res,
+           "e2e": {"value": v, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[2, 3, 4, 5])
+    ap.add_argument("--impl", default="bie", choices=["bie", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+/*
+ * bie.h -- C ABI of libbie.so, the B200 (sm_100a) fp64 implementation of the
+ * discretised Stokes boundary-integral-operator apply of Corona & Veerapaneni,
+ * "Boundary integral equation analysis for suspension of spheres in Stokes
+ * flow", arXiv 1707.06551.  P:n = PAPER.md line n; R<k> = reading k
+ * in DESIGN.md §3 (where the paper is garbled or silent).
+ *
+ * Conventions (all entry points)
+ *   - fp64 everywhere.  Vectors are [count][3] row-major, xyz interleaved.
+ *   - Node order (eq 4.2; R11): node i = s*(p+1)*(2p+2) + j*(2p+2) + k
+ *     for sphere s, polar index j (t_j = cos(theta_j) ascending Gauss-Legendre
+ *     nodes) and azimuthal index k (phi_k = 2 pi k/(2p+2)).
+ *   - Pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors on the
+ *     device current at bie_create) unless the name ends in _h (host).
+ *   - Streams: bie_stream_t is a cudaStream_t (NULL = legacy default stream).
+ *     Device-pointer calls are stream-ordered and return after enqueue; the
+ *     caller's buffers must stay valid until the stream reaches the work.
+ *     Asynchronous faults surface at the next synchronisation.  A context
+ *     holds scratch, so it must not be used from two streams concurrently;
+ *     distinct contexts are independent.
+ *   - Outputs are OVERWRITTEN, never accumulated.  An output that overlaps an
+ *     input returns BIE_ERR_ARG.
+ *   - Validation happens on the host at entry; kernels never check.  No C++
+ *     exception crosses the ABI.  On error the context's message
+ *     (bie_last_error) says which argument was wrong.
+ *   - Viscosity: PAPER sets nu = 1; here mu > 0 is a parameter (R5):
+ *     S velocity scales 1/mu, D velocity is mu-free, S pressure is mu-free,
+ *     D pressure scales mu.
+ */
+#ifndef BIE_H
+#define BIE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bie_ctx bie_ctx;
+typedef void* bie_stream_t; /* cudaStream_t */
+
+enum bie_status {
+  BIE_OK = 0,
+  BIE_ERR_ARG = 1,         /* bad pointer, size, value or aliasing          */
+  BIE_ERR_GEOMETRY = 2,    /* overlapping spheres (|c_i-c_j| < a_i + a_j)   */
+  BIE_ERR_ALLOC = 3,       /* device allocation failed                      */
+  BIE_ERR_CUDA = 4,        /* CUDA launch/runtime error                     */
+  BIE_ERR_UNSUPPORTED = 5  /* p outside [1, BIE_P_MAX] or no sm_100a device  */
+};
+
+#define BIE_P_MAX 30 /* self-term kernel keeps one sphere's spectra in shared memory */
+
+/* Parts selector for bie_apply_parts (testing / measurement). */
+#define BIE_PART_FAR 1  /* smooth Nystrom sum over all other spheres (a3)  */
+#define BIE_PART_SELF 2 /* spectral self term (a4-a6)                     */
+
+/* Kernel kinds reported by bie_get_profile. */
+#define BIE_KIND_SETUP 0    /* GL rule, Legendre/eigen tables, node generation (a1) */
+#define BIE_KIND_SELF 1     /* fused pack + forward VSHT + scale + inverse VSHT (a2, a4-a6) */
+#define BIE_KIND_PACK 2     /* source packing for off-surface evaluation (a2)   */
+#define BIE_KIND_NBODY 3    /* far-field SL+DL pair sum, self-sphere masked (a3) */
+#define BIE_KIND_REDUCE 4   /* deterministic reduction of source-chunk partials */
+#define BIE_KIND_OFFSURF 5  /* off-surface u,p pair sum (a7)                    */
+#define BIE_KIND_COPY 6     /* host<->device copies of the _host entry points   */
+#define BIE_NUM_KINDS 7
+
+/*
+ * bie_create -- build nodes, weights, normals and spectral tables (row a1).
+ *   centres_h [n_spheres][3], radii_h [n_spheres] : host, copied.
+ *   p  : quadrature/expansion order, grid (p+1) x (2p+2) per sphere (eq 4.2,
+ *        P:311), 1 <= p <= BIE_P_MAX.
+ *   mu : viscosity, finite and > 0.
+ *   Weights w = a^2 lambda_j 2 pi/(2p+2) (eq 4.4, reading R4);
+ *   outward normals.  Synchronous.  Returns BIE_ERR_ARG on NULL or
+ *   non-finite input, n_spheres < 1 or radii <= 0; BIE_ERR_GEOMETRY if two
+ *   spheres overlap (SPEC "no two spheres overlap", R19); BIE_ERR_UNSUPPORTED
+ *   for p out of range.  *out is NULL on failure.
+ */
+int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres, int p,
+               double mu, bie_ctx** out);
+
+/* bie_destroy -- frees everything the context owns.  NULL-safe. Synchronous. */
+void bie_destroy(bie_ctx* ctx);
+
+/* Number of nodes N = n_spheres (p+1)(2p+2); -1 for NULL. */
+int64_t bie_num_nodes(const bie_ctx* ctx);
+int bie_order(const bie_ctx* ctx);
+int64_t bie_num_spheres(const bie_ctx* ctx);
+
+/*
+ * bie_get_nodes -- copy node positions x [N][3], outward normals [N][3] and
+ * quadrature weights w [N] (device pointers; any may be NULL to skip) on s.
+ */
+int bie_get_nodes(const bie_ctx* ctx, double* x, double* normals, double* w, bie_stream_t s);
+
+/*
+ * bie_apply_SLDL -- u = S[f] + D_pv[q] at every node (rows a2-a6, the metric path).
+ *   S[f] (eq 2.19, 2.21), D[q] with the stresslet of eq 2.20 taken
+ *   with the sign fixed by the paper's spectra (reading R1): for node i of
+ *   sphere s
+ *     u_i = sum over nodes k of every OTHER sphere of
+ *             w_k [ (1/(8 pi mu)) (f_k/r + (rho.f_k) rho/r^3)
+ *                   + (3/(4 pi)) (rho.n_k)(rho.q_k) rho/r^5 ],  rho = x_i - x_k
+ *           (smooth rule eq 4.4 for all non-self pairs, "far-interactions with
+ *            the smooth quadrature" P:436; no near correction)
+ *         + the self term of sphere s: forward vector spherical harmonic
+ *           transform of (a_s/mu) f and q (discrete projection, R9), diagonal
+ *           scale by the S and principal-value D eigenvalues (Thm 2, P:217,
+ *           via eqs 3.6-3.11 at r -> 1, readings R2/R3), one inverse transform
+ *           (P:342).
+ *   No 1/2 I term is added (R14): D_pv is the principal value; the one-sided
+ *   limits are D_pv +- q/2, formed by the caller.
+ *   f, q, u : device [N][3].  u must not overlap f or q.
+ */
+int bie_apply_SLDL(bie_ctx* ctx, const double* f, const double* q, double* u, bie_stream_t s);
+
+/* bie_apply_SL -- u = S[f] (as bie_apply_SLDL with q = 0). */
+int bie_apply_SL(bie_ctx* ctx, const double* f, double* u, bie_stream_t s);
+
+/* bie_apply_DL -- u = D_pv[q] (as bie_apply_SLDL with f = 0). */
+int bie_apply_DL(bie_ctx* ctx, const double* q, double* u, bie_stream_t s);
+
+/*
+ * bie_apply_parts -- as bie_apply_SLDL restricted to `parts` (bitwise OR of
+ * BIE_PART_FAR and BIE_PART_SELF; 0 is BIE_ERR_ARG).  f or q may be NULL
+ * (zero density).  Used by the parity tests to check each row alone.
+ */
+int bie_apply_parts(bie_ctx* ctx, const double* f, const double* q, double* u, int parts,
+                    bie_stream_t s);
+
+/*
+ * bie_eval_offsurface -- velocity and pressure at m arbitrary targets (row a7).
+ *   u(x) = the smooth sum of bie_apply_SLDL over ALL nodes (no exclusion);
+ *   p(x) = sum_k w_k [ (1/(4 pi)) (rho.f_k)/r^3
+ *                      + (mu/(2 pi)) ( -(q_k.n_k)/r^3 + 3 (rho.q_k)(rho.n_k)/r^5 ) ]
+ *   (Stokeslet and stresslet pressures, reading R12; the paper's printed D
+ *   pressures P:215 are not used).  f or q may be NULL (zero density), p may
+ *   be NULL (not computed).  targets [m][3], u [m][3], p [m]: device.  Targets
+ *   closer to a surface than the smooth rule resolves are the caller's
+ *   contract (SPEC "garbage-in for non-separated targets"); a target that
+ *   coincides with a node gives inf/NaN.  m = 0 is a no-op.
+ */
+int bie_eval_offsurface(bie_ctx* ctx, const double* f, const double* q, const double* targets,
+                        int64_t m, double* u, double* p, bie_stream_t s);
+
+/*
+ * Host-buffer variants (end-to-end): identical results; the inputs are copied
+ * host->device on s (pinned host memory makes the copies asynchronous), the
+ * outputs device->host, and the call synchronises s before returning.
+ */
+int bie_apply_SLDL_host(bie_ctx* ctx, const double* f_h, const double* q_h, double* u_h,
+                        bie_stream_t s);
+int bie_eval_offsurface_host(bie_ctx* ctx, const double* f_h, const double* q_h,
+                             const double* targets_h, int64_t m, double* u_h, double* p_h,
+                             bie_stream_t s);
+
+/*
+ * Profiling: when enabled, every kernel the context launches is bracketed by
+ * CUDA events recorded on the launching stream.  bie_get_profile synchronises
+ * those events and returns, per kind (BIE_KIND_*), the cumulative device
+ * milliseconds and launch counts since the last reset.  Arrays have
+ * BIE_NUM_KINDS entries; either may be NULL.
+ */
+int bie_set_profiling(bie_ctx* ctx, int enable);
+int bie_get_profile(bie_ctx* ctx, double* ms, int64_t* launches);
+int bie_reset_profile(bie_ctx* ctx);
+
+/*
+ * Tuning knob: number of source chunks of the far-field kernel (0 = automatic;
+ * otherwise 1..4096).  Results are deterministic for a given value; different
+ * values change only the fp64 summation grouping.
+ */
+int bie_set_source_chunks(bie_ctx* ctx, int chunks);
+
+const char* bie_status_string(int status);
+const char* bie_last_error(const bie_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIE_H */

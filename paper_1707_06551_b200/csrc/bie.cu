@@ -1,0 +1,618 @@
+// bie.cu -- C ABI of libbie.so (declared and documented in include/bie.h).
+//
+// Host side: argument validation, device memory ownership, launch
+// configuration and profiling events.  Every arithmetic step of the path runs
+// in the kernels of k_setup.cuh, k_self.cuh and k_nbody.cuh.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/bie.h"
+#include "common.cuh"
+#include "k_nbody.cuh"
+#include "k_self.cuh"
+#include "k_setup.cuh"
+
+using namespace bie;
+
+namespace {
+
+// Far-field kernel configuration: R targets per thread,
+// TPB threads, TS sources per shared-memory tile, NST pipeline stages.
+constexpr int kR = 4, kTPB = 128, kTS = 64, kNST = 3;
+constexpr int kTgtTile = kR * kTPB;
+constexpr int64_t kOffBatch = 1 << 21;  // off-surface targets per batch (bounds scratch)
+constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
+
+#define NBODY_APPLY k_nbody<kR, kTPB, kTS, kNST, false>
+#define NBODY_OFF k_nbody<kR, kTPB, kTS, kNST, true>
+
+struct Ev {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct bie_ctx {
+  int dev = -1, sm_count = 0, occ_apply = 1, occ_off = 1;
+  int p = 0, nsn = 0;
+  int64_t ns = 0, N = 0;
+  double mu = 1.0;
+  double* d_centres = nullptr;
+  double* d_radii = nullptr;
+  double* d_tab = nullptr;
+  double* d_x = nullptr;
+  double* d_n = nullptr;
+  double* d_w = nullptr;
+  double* d_rec = nullptr;
+  double* d_qn3 = nullptr;
+  double* d_part = nullptr;
+  size_t part_cap = 0;  // doubles
+  int chunks_override = 0;
+  // staging for the _host entry points
+  double *d_f = nullptr, *d_q = nullptr, *d_u = nullptr;
+  double *d_tg = nullptr, *d_uo = nullptr, *d_po = nullptr;
+  int64_t tg_cap = 0;
+  // profiling
+  bool prof = false;
+  std::vector<Ev> pending;
+  double ms[BIE_NUM_KINDS] = {0};
+  int64_t launches[BIE_NUM_KINDS] = {0};
+  std::string err;
+};
+
+static int fail(bie_ctx* c, int st, const char* fmt, const char* a = "") {
+  if (c) {
+    char buf[512];
+    snprintf(buf, sizeof buf, fmt, a);
+    c->err = buf;
+  }
+  return st;
+}
+
+static int cuda_fail(bie_ctx* c, cudaError_t e, const char* where) {
+  if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return BIE_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- profiling
+static void prof_begin(bie_ctx* c, int kind, cudaStream_t s, Ev* ev) {
+  c->launches[kind]++;
+  ev->kind = kind;
+  ev->a = ev->b = nullptr;
+  if (!c->prof) return;
+  cudaEventCreate(&ev->a);
+  cudaEventCreate(&ev->b);
+  cudaEventRecord(ev->a, s);
+}
+
+static void prof_end(bie_ctx* c, cudaStream_t s, Ev* ev) {
+  if (!c->prof || !ev->a) return;
+  cudaEventRecord(ev->b, s);
+  c->pending.push_back(*ev);
+}
+
+static void prof_drain(bie_ctx* c) {
+  for (Ev& e : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(e.b);
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    c->ms[e.kind] += ms;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  c->pending.clear();
+}
+
+// ---------------------------------------------------------------- validation
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static bool overlaps(const double* a, int64_t na, const double* b, int64_t nb) {
+  if (!a || !b) return false;
+  return a < b + nb && b < a + na;
+}
+
+static int check_device(bie_ctx* c) {
+  int d = -1;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGetDevice");
+  if (d != c->dev) return fail(c, BIE_ERR_ARG, "current device differs from the device at bie_create%s");
+  return BIE_OK;
+}
+
+// Overlap test with a uniform cell list (cell = 2 max radius): O(n_spheres).
+static bool spheres_overlap(const double* c, const double* a, int64_t n, int64_t* bad_i, int64_t* bad_j) {
+  double amax = 0;
+  for (int64_t i = 0; i < n; ++i) amax = std::max(amax, a[i]);
+  const double h = 2.0 * amax;
+  auto key = [](int64_t x, int64_t y, int64_t z) {
+    return (uint64_t)((x & 0x1FFFFF) | ((y & 0x1FFFFF) << 21) | ((z & 0x1FFFFF) << 42));
+  };
+  std::unordered_map<uint64_t, std::vector<int64_t>> grid;
+  grid.reserve(2 * n);
+  std::vector<int64_t> cell(3 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < 3; ++d) cell[3 * i + d] = (int64_t)std::floor(c[3 * i + d] / h);
+    grid[key(cell[3 * i], cell[3 * i + 1], cell[3 * i + 2])].push_back(i);
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          auto it = grid.find(key(cell[3 * i] + dx, cell[3 * i + 1] + dy, cell[3 * i + 2] + dz));
+          if (it == grid.end()) continue;
+          for (int64_t j : it->second) {
+            if (j <= i) continue;
+            double r2 = 0;
+            for (int d = 0; d < 3; ++d) r2 += (c[3 * i + d] - c[3 * j + d]) * (c[3 * i + d] - c[3 * j + d]);
+            double lim = a[i] + a[j];
+            if (r2 < lim * lim) {
+              *bad_i = i;
+              *bad_j = j;
+              return true;
+            }
+          }
+        }
+  return false;
+}
+
+// ---------------------------------------------------------------- launches
+struct ChunkPlan {
+  int n_tt, n_chunks, tiles_per_chunk;
+};
+
+static ChunkPlan plan_chunks(const bie_ctx* c, int64_t M, int64_t N, int occ) {
+  ChunkPlan P;
+  P.n_tt = (int)((M + kTgtTile - 1) / kTgtTile);
+  const int64_t n_src_tiles = (N + kTS - 1) / kTS;
+  int64_t S;
+  if (c->chunks_override > 0) {
+    S = c->chunks_override;
+  } else {
+    const int64_t slots = (int64_t)c->sm_count * std::max(occ, 1);
+    S = (64 * slots + P.n_tt - 1) / P.n_tt;  // ~64 units per CTA slot: small tail
+    S = std::min<int64_t>(S, std::max<int64_t>(1, n_src_tiles / 4));
+    const int64_t cap = (int64_t)(kScratchBytes / (32.0 * std::max<int64_t>(M, 1)));
+    S = std::min<int64_t>(S, std::max<int64_t>(cap, 1));
+  }
+  S = std::max<int64_t>(1, std::min<int64_t>(S, n_src_tiles));
+  P.tiles_per_chunk = (int)((n_src_tiles + S - 1) / S);
+  P.n_chunks = (int)((n_src_tiles + P.tiles_per_chunk - 1) / P.tiles_per_chunk);
+  return P;
+}
+
+static int ensure_part(bie_ctx* c, size_t doubles) {
+  if (doubles <= c->part_cap) return BIE_OK;
+  if (c->d_part) cudaFree(c->d_part);
+  c->d_part = nullptr;
+  c->part_cap = 0;
+  cudaError_t e = cudaMalloc(&c->d_part, doubles * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, BIE_ERR_ALLOC, "cannot allocate far-field scratch%s");
+  }
+  c->part_cap = doubles;
+  return BIE_OK;
+}
+
+static int launch_check(bie_ctx* c, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, what);
+  return BIE_OK;
+}
+
+static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
+                     cudaStream_t s) {
+  // rows a2 + a4-a6: self term (or zeros) into u, packed sources into d_rec
+  SelfArgs SA;
+  SA.p = c->p;
+  SA.ns = c->ns;
+  SA.mu = c->mu;
+  SA.tab = c->d_tab;
+  SA.centres = c->d_centres;
+  SA.radii = c->d_radii;
+  SA.f = f;
+  SA.q = q;
+  SA.u = u;
+  SA.rec = c->d_rec;
+  SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
+  const size_t smem = self_smem_doubles(c->p) * sizeof(double);
+  Ev ev;
+  prof_begin(c, BIE_KIND_SELF, s, &ev);
+  k_self<<<(unsigned)c->ns, 256, smem, s>>>(SA);
+  prof_end(c, s, &ev);
+  int rc = launch_check(c, "k_self");
+  if (rc) return rc;
+  if (!(parts & BIE_PART_FAR)) return BIE_OK;
+  // row a3: far field
+  const ChunkPlan P = plan_chunks(c, c->N, c->N, c->occ_apply);
+  NbodyArgs A;
+  A.rec = c->d_rec;
+  A.qn3 = nullptr;
+  A.tx = nullptr;
+  A.N = c->N;
+  A.M = c->N;
+  A.nsn = c->nsn;
+  A.n_tt = P.n_tt;
+  A.n_chunks = P.n_chunks;
+  A.tiles_per_chunk = P.tiles_per_chunk;
+  A.pscale = 2.0 * c->mu;
+  A.pout = nullptr;
+  const size_t nb_smem = NbodySmem<kTS, kNST, false>::kBytes;
+  if (P.n_chunks == 1) {
+    A.uinit = u;
+    A.uout = u;
+    prof_begin(c, BIE_KIND_NBODY, s, &ev);
+    NBODY_APPLY<<<(unsigned)P.n_tt, kTPB, nb_smem, s>>>(A);
+    prof_end(c, s, &ev);
+    return launch_check(c, "k_nbody");
+  }
+  rc = ensure_part(c, (size_t)P.n_chunks * 3 * c->N);
+  if (rc) return rc;
+  A.uinit = nullptr;
+  A.uout = c->d_part;
+  prof_begin(c, BIE_KIND_NBODY, s, &ev);
+  NBODY_APPLY<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
+  prof_end(c, s, &ev);
+  rc = launch_check(c, "k_nbody");
+  if (rc) return rc;
+  prof_begin(c, BIE_KIND_REDUCE, s, &ev);
+  k_reduce<<<(unsigned)((3 * c->N + 255) / 256), 256, 0, s>>>(c->N, P.n_chunks, c->d_part, u, u,
+                                                               nullptr, nullptr, 0.0);
+  prof_end(c, s, &ev);
+  return launch_check(c, "k_reduce");
+}
+
+static int run_offsurface(bie_ctx* c, const double* f, const double* q, const double* tg,
+                          int64_t m, double* u, double* p, cudaStream_t s) {
+  if (m == 0) return BIE_OK;
+  Ev ev;
+  prof_begin(c, BIE_KIND_PACK, s, &ev);
+  k_pack<<<(unsigned)((c->N + 255) / 256), 256, 0, s>>>(c->p, c->N, c->mu, c->d_tab, c->d_centres,
+                                                        c->d_radii, f, q, c->d_rec, c->d_qn3);
+  prof_end(c, s, &ev);
+  int rc = launch_check(c, "k_pack");
+  if (rc) return rc;
+  const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
+  for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
+    const int64_t Mb = std::min(kOffBatch, m - b0);
+    const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_off);
+    NbodyArgs A;
+    A.rec = c->d_rec;
+    A.qn3 = c->d_qn3;
+    A.tx = tg + 3 * b0;
+    A.uinit = nullptr;
+    A.N = c->N;
+    A.M = Mb;
+    A.nsn = c->nsn;
+    A.n_tt = P.n_tt;
+    A.n_chunks = P.n_chunks;
+    A.tiles_per_chunk = P.tiles_per_chunk;
+    A.pscale = 2.0 * c->mu;
+    if (P.n_chunks == 1) {
+      A.uout = u + 3 * b0;
+      A.pout = p ? p + b0 : nullptr;
+      prof_begin(c, BIE_KIND_OFFSURF, s, &ev);
+      NBODY_OFF<<<(unsigned)P.n_tt, kTPB, nb_smem, s>>>(A);
+      prof_end(c, s, &ev);
+      rc = launch_check(c, "k_nbody_off");
+      if (rc) return rc;
+      continue;
+    }
+    rc = ensure_part(c, (size_t)P.n_chunks * 4 * Mb);
+    if (rc) return rc;
+    A.uout = c->d_part;
+    A.pout = p ? c->d_part + (size_t)P.n_chunks * 3 * Mb : nullptr;
+    prof_begin(c, BIE_KIND_OFFSURF, s, &ev);
+    NBODY_OFF<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
+    prof_end(c, s, &ev);
+    rc = launch_check(c, "k_nbody_off");
+    if (rc) return rc;
+    prof_begin(c, BIE_KIND_REDUCE, s, &ev);
+    k_reduce<<<(unsigned)((3 * Mb + 255) / 256), 256, 0, s>>>(
+        Mb, P.n_chunks, c->d_part, nullptr, u + 3 * b0, A.pout, p ? p + b0 : nullptr, 2.0 * c->mu);
+    prof_end(c, s, &ev);
+    rc = launch_check(c, "k_reduce");
+    if (rc) return rc;
+  }
+  return BIE_OK;
+}
+
+// ================================================================ ABI
+extern "C" {
+
+const char* bie_status_string(int st) {
+  switch (st) {
+    case BIE_OK: return "ok";
+    case BIE_ERR_ARG: return "invalid argument";
+    case BIE_ERR_GEOMETRY: return "overlapping spheres";
+    case BIE_ERR_ALLOC: return "device allocation failed";
+    case BIE_ERR_CUDA: return "CUDA error";
+    case BIE_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* bie_last_error(const bie_ctx* c) { return c ? c->err.c_str() : "NULL context"; }
+
+void bie_destroy(bie_ctx* c) {
+  if (!c) return;
+  prof_drain(c);
+  double* ptrs[] = {c->d_centres, c->d_radii, c->d_tab, c->d_x, c->d_n, c->d_w, c->d_rec,
+                    c->d_qn3, c->d_part, c->d_f, c->d_q, c->d_u, c->d_tg, c->d_uo, c->d_po};
+  for (double* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+}
+
+int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres, int p, double mu,
+               bie_ctx** out) {
+  if (!out) return BIE_ERR_ARG;
+  *out = nullptr;
+  if (!centres_h || !radii_h || n_spheres < 1) return BIE_ERR_ARG;
+  if (p < 1 || p > BIE_P_MAX) return BIE_ERR_UNSUPPORTED;
+  if (!(mu > 0.0) || !std::isfinite(mu)) return BIE_ERR_ARG;
+  for (int64_t i = 0; i < n_spheres; ++i) {
+    if (!(radii_h[i] > 0.0) || !std::isfinite(radii_h[i])) return BIE_ERR_ARG;
+    for (int d = 0; d < 3; ++d)
+      if (!std::isfinite(centres_h[3 * i + d])) return BIE_ERR_ARG;
+  }
+  int64_t bi, bj;
+  if (spheres_overlap(centres_h, radii_h, n_spheres, &bi, &bj)) return BIE_ERR_GEOMETRY;
+  const int nsn = (p + 1) * (2 * p + 2);
+  if (n_spheres > (int64_t)(INT32_MAX / nsn)) return BIE_ERR_UNSUPPORTED;  // int node indices
+
+  bie_ctx* c = new bie_ctx();
+  c->p = p;
+  c->nsn = nsn;
+  c->ns = n_spheres;
+  c->N = n_spheres * nsn;
+  c->mu = mu;
+  cudaError_t e = cudaGetDevice(&c->dev);
+  if (e != cudaSuccess) {
+    delete c;
+    cudaGetLastError();
+    return BIE_ERR_CUDA;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, c->dev);
+  if (prop.major != 10 || prop.minor != 0) {
+    delete c;
+    return BIE_ERR_UNSUPPORTED;
+  }
+  c->sm_count = prop.multiProcessorCount;
+  const TableLayout L(p);
+  auto alloc = [&](double** ptr, size_t n) -> bool {
+    return cudaMalloc(ptr, n * sizeof(double)) == cudaSuccess;
+  };
+  bool ok = alloc(&c->d_centres, 3 * n_spheres) && alloc(&c->d_radii, n_spheres) &&
+            alloc(&c->d_tab, L.total) && alloc(&c->d_x, 3 * c->N) && alloc(&c->d_n, 3 * c->N) &&
+            alloc(&c->d_w, c->N) && alloc(&c->d_rec, kRec * c->N + 2 * kRec) &&
+            alloc(&c->d_qn3, c->N + 2);
+  if (!ok) {
+    cudaGetLastError();
+    bie_destroy(c);
+    return BIE_ERR_ALLOC;
+  }
+  cudaMemcpy(c->d_centres, centres_h, 3 * n_spheres * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->d_radii, radii_h, n_spheres * sizeof(double), cudaMemcpyHostToDevice);
+  // row a1: GL rule -> tables -> nodes (default stream, synchronous)
+  Ev ev;
+  prof_begin(c, BIE_KIND_SETUP, 0, &ev);
+  k_gl_rule<<<1, 32>>>(p, c->d_tab);
+  k_tables<<<((p + 1) * (p + 1) + 127) / 128, 128>>>(p, c->d_tab);
+  k_nodes<<<(unsigned)((c->N + 255) / 256), 256>>>(p, c->N, c->d_tab, c->d_centres, c->d_radii,
+                                                  c->d_x, c->d_n, c->d_w);
+  c->launches[BIE_KIND_SETUP] += 2;
+  prof_end(c, 0, &ev);
+  const size_t smem = self_smem_doubles(p) * sizeof(double);
+  cudaFuncSetAttribute(k_self, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
+                                                NbodySmem<kTS, kNST, false>::kBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
+                                                NbodySmem<kTS, kNST, true>::kBytes);
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    bie_destroy(c);
+    return BIE_ERR_CUDA;
+  }
+  *out = c;
+  return BIE_OK;
+}
+
+int64_t bie_num_nodes(const bie_ctx* c) { return c ? c->N : -1; }
+int bie_order(const bie_ctx* c) { return c ? c->p : -1; }
+int64_t bie_num_spheres(const bie_ctx* c) { return c ? c->ns : -1; }
+
+int bie_get_nodes(const bie_ctx* cc, double* x, double* nrm, double* w, bie_stream_t s) {
+  bie_ctx* c = const_cast<bie_ctx*>(cc);
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)s;
+  const double* src[3] = {c->d_x, c->d_n, c->d_w};
+  double* dst[3] = {x, nrm, w};
+  const int64_t n[3] = {3 * c->N, 3 * c->N, c->N};
+  for (int k = 0; k < 3; ++k) {
+    if (!dst[k]) continue;
+    if (!is_device_ptr(dst[k])) return fail(c, BIE_ERR_ARG, "bie_get_nodes: output %s is not a device pointer", k == 0 ? "x" : (k == 1 ? "normals" : "w"));
+    cudaError_t e = cudaMemcpyAsync(dst[k], src[k], n[k] * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bie_get_nodes");
+  }
+  return BIE_OK;
+}
+
+int bie_apply_parts(bie_ctx* c, const double* f, const double* q, double* u, int parts,
+                    bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (parts <= 0 || parts > (BIE_PART_FAR | BIE_PART_SELF))
+    return fail(c, BIE_ERR_ARG, "parts must be a non-empty subset of FAR|SELF%s");
+  if (!u) return fail(c, BIE_ERR_ARG, "u is NULL%s");
+  const int64_t n3 = 3 * c->N;
+  if (!is_device_ptr(u)) return fail(c, BIE_ERR_ARG, "u is not a device pointer%s");
+  if (f && !is_device_ptr(f)) return fail(c, BIE_ERR_ARG, "f is not a device pointer%s");
+  if (q && !is_device_ptr(q)) return fail(c, BIE_ERR_ARG, "q is not a device pointer%s");
+  if (overlaps(u, n3, f, n3) || overlaps(u, n3, q, n3))
+    return fail(c, BIE_ERR_ARG, "output u overlaps an input%s");
+  return run_apply(c, f, q, u, parts, (cudaStream_t)s);
+}
+
+int bie_apply_SLDL(bie_ctx* c, const double* f, const double* q, double* u, bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  if (!f || !q) return fail(c, BIE_ERR_ARG, "bie_apply_SLDL: f and q must be non-NULL%s");
+  return bie_apply_parts(c, f, q, u, BIE_PART_FAR | BIE_PART_SELF, s);
+}
+
+int bie_apply_SL(bie_ctx* c, const double* f, double* u, bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  if (!f) return fail(c, BIE_ERR_ARG, "bie_apply_SL: f is NULL%s");
+  return bie_apply_parts(c, f, nullptr, u, BIE_PART_FAR | BIE_PART_SELF, s);
+}
+
+int bie_apply_DL(bie_ctx* c, const double* q, double* u, bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  if (!q) return fail(c, BIE_ERR_ARG, "bie_apply_DL: q is NULL%s");
+  return bie_apply_parts(c, nullptr, q, u, BIE_PART_FAR | BIE_PART_SELF, s);
+}
+
+int bie_eval_offsurface(bie_ctx* c, const double* f, const double* q, const double* tg, int64_t m,
+                        double* u, double* p, bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (m < 0) return fail(c, BIE_ERR_ARG, "m < 0%s");
+  if (m == 0) return BIE_OK;
+  if (!tg || !u) return fail(c, BIE_ERR_ARG, "targets and u must be non-NULL%s");
+  if (!is_device_ptr(tg) || !is_device_ptr(u) || (p && !is_device_ptr(p)) ||
+      (f && !is_device_ptr(f)) || (q && !is_device_ptr(q)))
+    return fail(c, BIE_ERR_ARG, "a buffer is not a device pointer%s");
+  const int64_t n3 = 3 * c->N;
+  if (overlaps(u, 3 * m, f, n3) || overlaps(u, 3 * m, q, n3) || overlaps(u, 3 * m, tg, 3 * m) ||
+      overlaps(p, m, f, n3) || overlaps(p, m, q, n3) || overlaps(p, m, tg, 3 * m) ||
+      overlaps(p, m, u, 3 * m))
+    return fail(c, BIE_ERR_ARG, "an output overlaps an input or the other output%s");
+  return run_offsurface(c, f, q, tg, m, u, p, (cudaStream_t)s);
+}
+
+static int stage(bie_ctx* c, double** d, size_t n) {
+  if (*d) return BIE_OK;
+  if (cudaMalloc(d, n * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, BIE_ERR_ALLOC, "cannot allocate staging buffers%s");
+  }
+  return BIE_OK;
+}
+
+int bie_apply_SLDL_host(bie_ctx* c, const double* f_h, const double* q_h, double* u_h,
+                        bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (!f_h || !q_h || !u_h) return fail(c, BIE_ERR_ARG, "host buffers must be non-NULL%s");
+  const size_t n3 = 3 * c->N;
+  if ((rc = stage(c, &c->d_f, n3)) || (rc = stage(c, &c->d_q, n3)) || (rc = stage(c, &c->d_u, n3)))
+    return rc;
+  cudaStream_t st = (cudaStream_t)s;
+  Ev ev;
+  prof_begin(c, BIE_KIND_COPY, st, &ev);
+  cudaMemcpyAsync(c->d_f, f_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->d_q, q_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  prof_end(c, st, &ev);
+  rc = run_apply(c, c->d_f, c->d_q, c->d_u, BIE_PART_FAR | BIE_PART_SELF, st);
+  if (rc) return rc;
+  prof_begin(c, BIE_KIND_COPY, st, &ev);
+  cudaMemcpyAsync(u_h, c->d_u, n3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  prof_end(c, st, &ev);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "bie_apply_SLDL_host");
+  return BIE_OK;
+}
+
+int bie_eval_offsurface_host(bie_ctx* c, const double* f_h, const double* q_h, const double* tg_h,
+                             int64_t m, double* u_h, double* p_h, bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (m < 0) return fail(c, BIE_ERR_ARG, "m < 0%s");
+  if (m == 0) return BIE_OK;
+  if (!tg_h || !u_h) return fail(c, BIE_ERR_ARG, "targets and u must be non-NULL%s");
+  const size_t n3 = 3 * c->N;
+  if ((f_h && (rc = stage(c, &c->d_f, n3))) || (q_h && (rc = stage(c, &c->d_q, n3)))) return rc;
+  if (m > c->tg_cap) {
+    cudaFree(c->d_tg);
+    cudaFree(c->d_uo);
+    cudaFree(c->d_po);
+    c->d_tg = c->d_uo = c->d_po = nullptr;
+    c->tg_cap = 0;
+    if ((rc = stage(c, &c->d_tg, 3 * m)) || (rc = stage(c, &c->d_uo, 3 * m)) ||
+        (rc = stage(c, &c->d_po, m)))
+      return rc;
+    c->tg_cap = m;
+  }
+  cudaStream_t st = (cudaStream_t)s;
+  Ev ev;
+  prof_begin(c, BIE_KIND_COPY, st, &ev);
+  if (f_h) cudaMemcpyAsync(c->d_f, f_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (q_h) cudaMemcpyAsync(c->d_q, q_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->d_tg, tg_h, 3 * m * sizeof(double), cudaMemcpyHostToDevice, st);
+  prof_end(c, st, &ev);
+  rc = run_offsurface(c, f_h ? c->d_f : nullptr, q_h ? c->d_q : nullptr, c->d_tg, m, c->d_uo,
+                      p_h ? c->d_po : nullptr, st);
+  if (rc) return rc;
+  prof_begin(c, BIE_KIND_COPY, st, &ev);
+  cudaMemcpyAsync(u_h, c->d_uo, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (p_h) cudaMemcpyAsync(p_h, c->d_po, m * sizeof(double), cudaMemcpyDeviceToHost, st);
+  prof_end(c, st, &ev);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "bie_eval_offsurface_host");
+  return BIE_OK;
+}
+
+int bie_set_profiling(bie_ctx* c, int enable) {
+  if (!c) return BIE_ERR_ARG;
+  c->prof = enable != 0;
+  return BIE_OK;
+}
+
+int bie_get_profile(bie_ctx* c, double* ms, int64_t* launches) {
+  if (!c) return BIE_ERR_ARG;
+  prof_drain(c);
+  for (int k = 0; k < BIE_NUM_KINDS; ++k) {
+    if (ms) ms[k] = c->ms[k];
+    if (launches) launches[k] = c->launches[k];
+  }
+  return BIE_OK;
+}
+
+int bie_reset_profile(bie_ctx* c) {
+  if (!c) return BIE_ERR_ARG;
+  prof_drain(c);
+  for (int k = 0; k < BIE_NUM_KINDS; ++k) {
+    c->ms[k] = 0;
+    c->launches[k] = 0;
+  }
+  return BIE_OK;
+}
+
+int bie_set_source_chunks(bie_ctx* c, int chunks) {
+  if (!c) return BIE_ERR_ARG;
+  if (chunks < 0 || chunks > 4096) return fail(c, BIE_ERR_ARG, "chunks must be in [0, 4096]%s");
+  c->chunks_override = chunks;
+  return BIE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+// k_nbody.cuh -- fused Stokeslet + stresslet fp64 N-body sum (rows a3, a7).
+//
+// u_i += sum_k y_k [ f'_k + rho (rho.f'_k + (rho.n_k)(rho.q'_k) y_k^2) y_k^2 ],
+//   rho = x_i - x_k, y_k = 1/|rho|, f' = w f/(8 pi mu), q' = (3/(4 pi)) w q,
+// which is S[f] (eq 2.19) + D[q] (eq 2.20 with sign reading R1) under the
+// smooth rule (eq 4.4).  30 FP64 pipe instructions per pair (18 DFMA, 9 DMUL,
+// 3 DADD); the reciprocal square root is a MUFU seed plus one third-order
+// fp64 refinement y = y0 + y0 e (1/2 + 3/8 e), e = 1 - r^2 y0^2.
+// Off-surface (a7) adds the pressure p += (t2 - qn3_k) y^3 (2 more ops).
+//
+// Decomposition: CTA = (target tile of TPB*R targets, source chunk).  Source
+// tiles of TS packed records (96 B each) stream global -> shared through the
+// TMA bulk-copy unit into an NST-deep ring guarded by mbarriers; every thread
+// holds R targets in registers and reads each source once from shared memory
+// (broadcast LDS.128).  Self-sphere exclusion (reading R8) is a per-pair
+// select applied only in source tiles that overlap the CTA's own spheres.
+// Chunk partials are reduced in fixed order by k_reduce (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace bie {
+
+struct NbodyArgs {
+  const double* rec;    // [N][kRec] sources
+  const double* qn3;    // [N (+pad)] (off-surface pressure only)
+  const double* tx;     // [M][3] targets (off-surface) or nullptr (targets = source nodes)
+  const double* uinit;  // [M][3] added when n_chunks == 1 (self term), may be nullptr
+  double* uout;         // n_chunks == 1: [M][3] final; else partial base [n_chunks][M][3]
+  double* pout;         // off-surface: n_chunks == 1: [M]; else [n_chunks][M]; may be nullptr
+  int64_t N;            // number of sources
+  int64_t M;            // number of targets
+  int nsn;              // nodes per sphere (masking)
+  int n_tt;             // target tiles
+  int n_chunks;         // source chunks
+  int tiles_per_chunk;  // source tiles per chunk
+  double pscale;        // 2 mu (pressure)
+};
+
+template <int TS, int NST, bool OFF>
+struct NbodySmem {
+  static constexpr int kRecBytes = TS * kRec * 8;
+  static constexpr int kQnBytes = OFF ? TS * 8 : 0;
+  static constexpr int kStageBytes = kRecBytes + kQnBytes;
+  static constexpr int kBytes = NST * kStageBytes + NST * 8;
+};
+
+template <bool MASK, bool OFF>
+__device__ __forceinline__ void pair_acc(const double2 s0, const double2 s1, const double2 s2,
+                                         const double2 s3, const double2 s4, const double2 s5,
+                                         double qn, const double* xt, double* acc, double& pacc,
+                                         int k, int lo, int nsn) {
+  // s0=(x0,x1) s1=(x2,n0) s2=(n1,n2) s3=(f0,f1) s4=(f2,q0) s5=(q1,q2)
+  const double dx = xt[0] - s0.x, dy = xt[1] - s0.y, dz = xt[2] - s1.x;
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  double y = fma(y0 * e, fma(e, 0.375, 0.5), y0);
+  if (MASK) {
+    if ((unsigned)(k - lo) < (unsigned)nsn) y = 0.0;  // own sphere: excluded (R8)
+  }
+  const double rf = fma(dz, s4.x, fma(dy, s3.y, dx * s3.x));
+  const double rn = fma(dz, s2.y, fma(dy, s2.x, dx * s1.y));
+  const double rq = fma(dz, s5.y, fma(dy, s5.x, dx * s4.y));
+  const double y2 = y * y;
+  const double t2 = fma(rn * rq, y2, rf);
+  const double sp = t2 * y2;
+  acc[0] = fma(y, fma(dx, sp, s3.x), acc[0]);
+  acc[1] = fma(y, fma(dy, sp, s3.y), acc[1]);
+  acc[2] = fma(y, fma(dz, sp, s4.x), acc[2]);
+  if (OFF) pacc = fma(fma(-qn, y2, sp), y, pacc);
+}
+
+template <int R, int TPB, int TS, int NST, bool OFF>
+__global__ void __launch_bounds__(TPB) k_nbody(const NbodyArgs A) {
+  using SM = NbodySmem<TS, NST, OFF>;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + NST * SM::kStageBytes);
+
+  const int tt = blockIdx.x % A.n_tt;
+  const int chunk = blockIdx.x / A.n_tt;
+  const int64_t n_src_tiles = (A.N + TS - 1) / TS;
+  const int64_t tile0 = (int64_t)chunk * A.tiles_per_chunk;
+  int ntile = (int)min((int64_t)A.tiles_per_chunk, n_src_tiles - tile0);
+  if (ntile < 0) ntile = 0;
+
+  // ---- targets held in registers
+  double xt[R][3], acc[R][3], pacc[R];
+  int lo[R];
+  int64_t tidx[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t i = (int64_t)tt * TPB * R + r * TPB + threadIdx.x;
+    tidx[r] = i;
+    const int64_t ic = i < A.M ? i : A.M - 1;
+    if (OFF) {
+      xt[r][0] = A.tx[3 * ic];
+      xt[r][1] = A.tx[3 * ic + 1];
+      xt[r][2] = A.tx[3 * ic + 2];
+      lo[r] = 0;
+    } else {
+      xt[r][0] = A.rec[ic * kRec];
+      xt[r][1] = A.rec[ic * kRec + 1];
+      xt[r][2] = A.rec[ic * kRec + 2];
+      lo[r] = (int)((ic / A.nsn) * A.nsn);
+    }
+    acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+    pacc[r] = 0.0;
+  }
+  // CTA-uniform node range of the spheres owning this tile's targets
+  int64_t first = (int64_t)tt * TPB * R;
+  int64_t last = min(first + TPB * R, A.M) - 1;
+  const int64_t cta_lo = (first / A.nsn) * A.nsn;
+  const int64_t cta_hi = (last / A.nsn + 1) * A.nsn;
+
+  auto issue = [&](int it) {
+    const int st = it % NST;
+    const int64_t k0 = (tile0 + it) * TS;
+    const int cnt = (int)min((int64_t)TS, A.N - k0);
+    unsigned char* base = smraw + st * SM::kStageBytes;
+    uint32_t bytes = cnt * kRec * 8;
+    uint32_t qbytes = OFF ? ((cnt + 1) & ~1) * 8 : 0;
+    mbar_arrive_expect_tx(&bar[st], bytes + qbytes);
+    bulk_g2s(base, A.rec + k0 * kRec, bytes, &bar[st]);
+    if (OFF) bulk_g2s(base + SM::kRecBytes, A.qn3 + k0, qbytes, &bar[st]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < NST; ++st) mbar_init(&bar[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int it = 0; it < NST && it < ntile; ++it) issue(it);
+  }
+
+  for (int it = 0; it < ntile; ++it) {
+    const int st = it % NST;
+    mbar_wait(&bar[st], (it / NST) & 1);
+    const int64_t k0 = (tile0 + it) * TS;
+    const int cnt = (int)min((int64_t)TS, A.N - k0);
+    const double2* srec = reinterpret_cast<const double2*>(smraw + st * SM::kStageBytes);
+    const double* sqn = reinterpret_cast<const double*>(smraw + st * SM::kStageBytes + SM::kRecBytes);
+    const bool masked = !OFF && (k0 < cta_hi) && (k0 + cnt > cta_lo);
+    if (!masked) {
+#pragma unroll 2
+      for (int sidx = 0; sidx < cnt; ++sidx) {
+        const double2* sr = srec + sidx * (kRec / 2);
+        const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
+        const double qn = OFF ? sqn[sidx] : 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          pair_acc<false, OFF>(s0, s1, s2, s3, s4, s5, qn, xt[r], acc[r], pacc[r], 0, 0, 1);
+      }
+    } else {
+      for (int sidx = 0; sidx < cnt; ++sidx) {
+        const double2* sr = srec + sidx * (kRec / 2);
+        const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
+        const int k = (int)(k0 + sidx);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], k, lo[r],
+                                A.nsn);
+      }
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (threadIdx.x == 0 && it + NST < ntile) issue(it + NST);
+  }
+
+  // ---- epilogue
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t i = tidx[r];
+    if (i >= A.M) continue;
+    const int64_t li = i;
+    if (A.n_chunks == 1) {
+      double u0 = acc[r][0], u1 = acc[r][1], u2 = acc[r][2];
+      if (A.uinit) {
+        u0 += A.uinit[3 * i];
+        u1 += A.uinit[3 * i + 1];
+        u2 += A.uinit[3 * i + 2];
+      }
+      A.uout[3 * li] = u0;
+      A.uout[3 * li + 1] = u1;
+      A.uout[3 * li + 2] = u2;
+      if (OFF && A.pout) A.pout[li] = A.pscale * pacc[r];
+    } else {
+      const int64_t Mb = A.M;
+      double* po = A.uout + ((int64_t)chunk * Mb + li) * 3;
+      po[0] = acc[r][0];
+      po[1] = acc[r][1];
+      po[2] = acc[r][2];
+      if (OFF && A.pout) A.pout[(int64_t)chunk * Mb + li] = pacc[r];
+    }
+  }
+}
+
+// u[i] = (uinit ? uinit[i] : 0) + sum_{c < n_chunks} part[c][i], fixed order;
+// pressure likewise, scaled by pscale.  One thread per target component.
+__global__ void k_reduce(int64_t Mb, int n_chunks, const double* __restrict__ part,
+                         const double* __restrict__ uinit, double* __restrict__ u,
+                         const double* __restrict__ ppart, double* __restrict__ p, double pscale) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < 3 * Mb) {
+    double s = 0.0;
+    for (int c = 0; c < n_chunks; ++c) s += part[(int64_t)c * 3 * Mb + e];
+    u[e] = uinit ? uinit[e] + s : s;
+  }
+  if (ppart && p && e < Mb) {
+    double s = 0.0;
+    for (int c = 0; c < n_chunks; ++c) s += ppart[(int64_t)c * Mb + e];
+    p[e] = pscale * s;
+  }
+}
+
+}  // namespace bie

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by
+element on the same seeded inputs.  Bar (BASELINE.json north_star): relative
+L2 <= 1e-12 and max |delta| / max |u_ref| <= 1e-10 in fp64.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-12
+MAX_REL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def bie():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1707_06551_b200 as m
+    return m
+
+
+def _err(got, ref):
+    got, ref = np.asarray(got), np.asarray(ref)
+    return (np.linalg.norm(got - ref) / np.linalg.norm(ref),
+            np.abs(got - ref).max() / np.abs(ref).max())
+
+
+def _assert_parity(got, ref, what=""):
+    rel, mx = _err(got, ref)
+    assert rel <= REL_L2 and mx <= MAX_REL, f"{what}: rel-L2 {rel:.3e} max {mx:.3e}"
+
+
+def _dev(a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def gpu_apply(bie, centres, radii, p, mu, f, q, parts=3, chunks=0):
+    ctx = bie.bie_create(centres, radii, p, mu)
+    if chunks:
+        bie.bie_set_source_chunks(ctx, chunks)
+    N = bie.bie_num_nodes(ctx)
+    u = torch.full((N, 3), np.nan, dtype=torch.float64, device="cuda")
+    bie.bie_apply_parts(ctx, _dev(f), _dev(q), u, parts)
+    torch.cuda.synchronize()
+    ctx.close()
+    return u.cpu().numpy()
+
+
+def _random_case(seed, ns, p, poly=True, mu=1.0):
+    """Small random suspension (not a BASELINE config): RSA-like placement."""
+    rng = np.random.default_rng(seed)
+    radii = rng.uniform(0.5, 1.5, ns) if poly else np.ones(ns)
+    c = []
+    while len(c) < ns:
+        x = rng.uniform(0, 4.0 * ns ** (1 / 3) + 3, 3)
+        i = len(c)
+        if all(np.linalg.norm(x - y) >= radii[i] + radii[j] + 0.3 for j, y in enumerate(c)):
+            c.append(x)
+    N = ns * (p + 1) * (2 * p + 2)
+    return np.array(c), radii, rng.standard_normal((N, 3)), rng.standard_normal((N, 3)), mu
+
+
+# ------------------------------------------------------------------- a1
+@pytest.mark.parametrize("p", [1, 4, 12, 30])
+def test_nodes_match_oracle(bie, oracle_mod, p):
+    c, a, _, _, _ = _random_case(p, 5, p)
+    ctx = bie.bie_create(c, a, p, 1.0)
+    N = bie.bie_num_nodes(ctx)
+    x = torch.empty((N, 3), dtype=torch.float64, device="cuda")
+    n = torch.empty_like(x)
+    w = torch.empty(N, dtype=torch.float64, device="cuda")
+    bie.bie_get_nodes(ctx, x, n, w)
+    torch.cuda.synchronize()
+    xr, nr, wr = oracle_mod.nodes(c, a, p)
+    assert np.abs(x.cpu().numpy() - xr).max() <= 4e-15 * np.abs(xr).max()
+    assert np.abs(n.cpu().numpy() - nr).max() <= 2e-15
+    assert np.abs(w.cpu().numpy() / wr - 1).max() <= 4e-14
+    ctx.close()
+
+
+# --------------------------------------------------------- a4-a6 self term
+@pytest.mark.parametrize("p,ns,poly,mu", [(1, 3, True, 1.0), (4, 2, False, 1.0), (8, 4, True, 1.7),
+                                          (12, 2, True, 0.6), (16, 1, False, 1.0), (30, 1, True, 2.0)])
+def test_self_term_only(bie, oracle_mod, p, ns, poly, mu):
+    c, a, f, q, mu = _random_case(100 + p, ns, p, poly, mu)
+    ref = oracle_mod.self_term(c, a, p, mu, f, q)
+    got = gpu_apply(bie, c, a, p, mu, f, q, parts=bie.BIE_PART_SELF)
+    _assert_parity(got, ref, f"self p={p}")
+
+
+# ------------------------------------------------------------- a3 far field
+@pytest.mark.parametrize("p,ns,chunks", [(4, 2, 0), (4, 7, 3), (6, 9, 0), (8, 5, 1), (5, 3, 2)])
+def test_far_field_only(bie, oracle_mod, p, ns, chunks):
+    c, a, f, q, mu = _random_case(200 + p + ns, ns, p, True, 1.3)
+    ref = oracle_mod.far(c, a, p, mu, f, q)
+    got = gpu_apply(bie, c, a, p, mu, f, q, parts=bie.BIE_PART_FAR, chunks=chunks)
+    _assert_parity(got, ref, f"far p={p} ns={ns} chunks={chunks}")
+
+
+def test_single_sphere_far_field_is_zero(bie):
+    c, a, f, q, mu = _random_case(7, 1, 6)
+    got = gpu_apply(bie, c, a, 6, mu, f, q, parts=bie.BIE_PART_FAR)
+    assert np.all(got == 0.0)
+
+
+# ------------------------------------------------------- BASELINE configs
+def _cfg_inputs(oracle_mod, cfg):
+    from bie_inputs import make_config, rigid_field
+    d = make_config(cfg, with_targets=(cfg == 5))
+    f, q = d["f"], d["q"]
+    if d["rigid"] is not None:
+        x, _, _ = oracle_mod.nodes(d["centres"], d["radii"], d["p"])
+        q = rigid_field(*d["rigid"], x, d["centres"], (d["p"] + 1) * (2 * d["p"] + 2))
+    if d["same_fq"]:
+        f = q
+    return d, f, q
+
+
+def test_config1_full(bie, oracle_mod):
+    d, f, q = _cfg_inputs(oracle_mod, 1)
+    ref = oracle_mod.apply(d["centres"], d["radii"], d["p"], d["mu"], f, q)
+    got = gpu_apply(bie, d["centres"], d["radii"], d["p"], d["mu"], f, q)
+    _assert_parity(got, ref, "cfg1")
+    # SL only / DL only through their own entry points
+    ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
+    u = torch.empty((100, 3), dtype=torch.float64, device="cuda")
+    bie.bie_apply_SL(ctx, _dev(f), u)
+    _assert_parity(u.cpu().numpy(), oracle_mod.apply(d["centres"], d["radii"], 4, 1.0, f, None), "SL")
+    bie.bie_apply_DL(ctx, _dev(q), u)
+    _assert_parity(u.cpu().numpy(), oracle_mod.apply(d["centres"], d["radii"], 4, 1.0, None, q), "DL")
+    ctx.close()
+
+
+def test_config2_full(bie, oracle_mod):
+    d, f, q = _cfg_inputs(oracle_mod, 2)
+    ref = oracle_mod.apply(d["centres"], d["radii"], d["p"], d["mu"], f, q)
+    got = gpu_apply(bie, d["centres"], d["radii"], d["p"], d["mu"], f, q)
+    _assert_parity(got, ref, "cfg2")
+
+
+@pytest.mark.parametrize("cfg,nsub", [(3, 2048), (4, 256), (5, 384)])
+def test_config_subset(bie, oracle_mod, cfg, nsub):
+    """Full-size configs in the launch configuration bench.py times; oracle on a
+    sorted prefix of the seeded 4096-node subset (sizes keep the CPU time bounded)."""
+    d, f, q = _cfg_inputs(oracle_mod, cfg)
+    sub = d["subset"][np.linspace(0, len(d["subset"]) - 1, nsub).astype(int)]
+    got = gpu_apply(bie, d["centres"], d["radii"], d["p"], d["mu"], f, q)[sub]
+    ref = oracle_mod.apply(d["centres"], d["radii"], d["p"], d["mu"], f, q, sub)
+    _assert_parity(got, ref, f"cfg{cfg}")
+
+
+def test_config5_offsurface_subset(bie, oracle_mod):
+    d, f, q = _cfg_inputs(oracle_mod, 5)
+    tsub = d["target_subset"][::8]
+    ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
+    tg = _dev(d["targets"])
+    M = tg.shape[0]
+    u = torch.empty((M, 3), dtype=torch.float64, device="cuda")
+    p = torch.empty(M, dtype=torch.float64, device="cuda")
+    bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), tg, u, p)
+    torch.cuda.synchronize()
+    uref, pref = oracle_mod.offsurface(d["centres"], d["radii"], d["p"], d["mu"], f, q,
+                                       d["targets"][tsub])
+    _assert_parity(u.cpu().numpy()[tsub], uref, "cfg5 offsurface u")
+    _assert_parity(p.cpu().numpy()[tsub], pref, "cfg5 offsurface p")
+    ctx.close()
+
+
+# --------------------------------------------------------- a7 off-surface
+@pytest.mark.parametrize("use_f,use_q,use_p", [(True, True, True), (True, False, True),
+                                               (False, True, False)])
+def test_offsurface_small(bie, oracle_mod, use_f, use_q, use_p):
+    c, a, f, q, mu = _random_case(11, 4, 5, True, 0.8)
+    rng = np.random.default_rng(12)
+    tg = rng.uniform(-3, 10, (1000, 3))
+    dmin = np.min(np.linalg.norm(tg[:, None] - c[None], axis=-1) - a[None], axis=1)
+    tg = tg[np.abs(dmin) > 0.3]
+    fx, qx = (f if use_f else None), (q if use_q else None)
+    uref, pref = oracle_mod.offsurface(c, a, 5, mu, fx, qx, tg)
+    ctx = bie.bie_create(c, a, 5, mu)
+    M = len(tg)
+    u = torch.empty((M, 3), dtype=torch.float64, device="cuda")
+    p = torch.empty(M, dtype=torch.float64, device="cuda") if use_p else None
+    bie.bie_eval_offsurface(ctx, _dev(fx), _dev(qx), _dev(tg), u, p)
+    torch.cuda.synchronize()
+    _assert_parity(u.cpu().numpy(), uref, "offsurface u")
+    if use_p:
+        _assert_parity(p.cpu().numpy(), pref, "offsurface p")
+    # zero targets is a no-op
+    bie.bie_eval_offsurface(ctx, _dev(fx), _dev(qx), torch.empty((0, 3), dtype=torch.float64,
+                                                                   device="cuda"),
+                            torch.empty((0, 3), dtype=torch.float64, device="cuda"))
+    ctx.close()
+
+
+# ---------------------------------------------------- determinism, e2e, ABI
+def test_determinism_and_host_entry_point(bie, oracle_mod):
+    d, f, q = _cfg_inputs(oracle_mod, 2)
+    u1 = gpu_apply(bie, d["centres"], d["radii"], d["p"], d["mu"], f, q)
+    u2 = gpu_apply(bie, d["centres"], d["radii"], d["p"], d["mu"], f, q)
+    assert np.array_equal(u1, u2)
+    ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
+    uh = np.empty_like(f)
+    bie.bie_apply_SLDL_host(ctx, np.ascontiguousarray(f), np.ascontiguousarray(q), uh)
+    assert np.array_equal(uh, u1)
+    ctx.close()
+
+
+def test_chunking_changes_only_rounding(bie, oracle_mod):
+    c, a, f, q, mu = _random_case(31, 6, 7, True, 1.0)
+    ref = oracle_mod.apply(c, a, 7, mu, f, q)
+    for ch in (1, 2, 5, 11):
+        _assert_parity(gpu_apply(bie, c, a, 7, mu, f, q, chunks=ch), ref, f"chunks={ch}")
+
+
+def test_abi_errors_on_gpu(bie):
+    c, a, f, q, mu = _random_case(41, 2, 4)
+    ctx = bie.bie_create(c, a, 4, mu)
+    fd, qd = _dev(f), _dev(q)
+    with pytest.raises(bie.BieError) as e:
+        bie.bie_apply_SLDL(ctx, fd, qd, fd)           # output aliases input
+    assert e.value.status == bie.BIE_ERR_ARG
+    from paper_1707_06551_b200 import _abi
+    u = torch.empty_like(fd)
+    rc = _abi._lib.bie_apply_SLDL(ctx.handle, f.ctypes.data, qd.data_ptr(), u.data_ptr(), None)
+    assert rc == bie.BIE_ERR_ARG                      # host pointer where device expected
+    rc = _abi._lib.bie_apply_parts(ctx.handle, fd.data_ptr(), qd.data_ptr(), u.data_ptr(), 0, None)
+    assert rc == bie.BIE_ERR_ARG
+    assert "parts" in bie.bie_last_error(ctx)
+    ctx.close()
+
+
+def test_streams_and_two_contexts(bie, oracle_mod):
+    c1, a1, f1, q1, mu1 = _random_case(51, 3, 4)
+    c2, a2, f2, q2, mu2 = _random_case(52, 4, 6)
+    r1 = oracle_mod.apply(c1, a1, 4, mu1, f1, q1)
+    r2 = oracle_mod.apply(c2, a2, 6, mu2, f2, q2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    k1, k2 = bie.bie_create(c1, a1, 4, mu1), bie.bie_create(c2, a2, 6, mu2)
+    u1 = torch.empty((len(f1), 3), dtype=torch.float64, device="cuda")
+    u2 = torch.empty((len(f2), 3), dtype=torch.float64, device="cuda")
+    F1, Q1, F2, Q2 = _dev(f1), _dev(q1), _dev(f2), _dev(q2)
+    torch.cuda.synchronize()
+    bie.bie_apply_SLDL(k1, F1, Q1, u1, stream=s1)
+    bie.bie_apply_SLDL(k2, F2, Q2, u2, stream=s2)
+    torch.cuda.synchronize()
+    _assert_parity(u1.cpu().numpy(), r1, "ctx1")
+    _assert_parity(u2.cpu().numpy(), r2, "ctx2")
+    k1.close()
+    k2.close()
+
+
+def test_smoke_entry(bie):
+    import __graft_entry__
+    __graft_entry__.smoke()
