@@ -209,7 +209,7 @@ def run_gpu(args):
     peak = peak_fp64_tflops()
     roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "k_nbody<4,128,64,3,false> (far-field SL+DL, row a3)",
+                "kernel": "k_nbody<8,64,64,3,false> (far-field SL+DL, row a3)",
                 "peak_source": "derived: 148 SM x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (DESIGN.md §5)",
                 "fp64_pipe_frac": round(nb_pairs_s * FP64_OPS_PER_PAIR / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)}
     if clk.get("sm_mhz"):

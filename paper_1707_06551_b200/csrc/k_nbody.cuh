@@ -54,7 +54,9 @@ __device__ __forceinline__ void pair_acc(const double2 s0, const double2 s1, con
   const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
   const double y0 = rsqrt_seed(r2);
   const double e = fma(-r2, y0 * y0, 1.0);
-  double y = fma(y0 * e, fma(e, 0.375, 0.5), y0);
+  // y = y0 (1 + e (1/2 + 3/8 e)): every DFMA here has an immediate operand, so
+  // none needs three fresh 64-bit register reads (RF model).
+  double y = y0 * fma(e, fma(e, 0.375, 0.5), 1.0);
   if (MASK) {
     if ((unsigned)(k - lo) < (unsigned)nsn) y = 0.0;  // own sphere: excluded (R8)
   }
@@ -70,8 +72,8 @@ __device__ __forceinline__ void pair_acc(const double2 s0, const double2 s1, con
   if (OFF) pacc = fma(fma(-qn, y2, sp), y, pacc);
 }
 
-template <int R, int TPB, int TS, int NST, bool OFF>
-__global__ void __launch_bounds__(TPB) k_nbody(const NbodyArgs A) {
+template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2>
+__global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   using SM = NbodySmem<TS, NST, OFF>;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + NST * SM::kStageBytes);
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(TPB) k_nbody(const NbodyArgs A) {
     const double* sqn = reinterpret_cast<const double*>(smraw + st * SM::kStageBytes + SM::kRecBytes);
     const bool masked = !OFF && (k0 < cta_hi) && (k0 + cnt > cta_lo);
     if (!masked) {
-#pragma unroll 2
+#pragma unroll(UNR)
       for (int sidx = 0; sidx < cnt; ++sidx) {
         const double2* sr = srec + sidx * (kRec / 2);
         const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
