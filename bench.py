@@ -207,8 +207,19 @@ def run_gpu(args):
     nb_pairs_s = apply_pairs / (nb_ms / 1e3)
     achieved = nb_pairs_s * FLOPS_PER_PAIR / 1e12
     peak = peak_fp64_tflops()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"cfg{args.config}")
+        if tr:
+            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+    except Exception:
+        pass
     roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_note": "DRAM bytes per launch from profiles/traffic.json (ncu --set full); "
+                                "algorithmic bytes: 96 B/source record + 24 B/target = "
+                                f"{(96 + 24) * N} B",
                 "kernel": "k_nbody<8,64,64,3,false> (far-field SL+DL, row a3)",
                 "peak_source": "derived: 148 SM x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (DESIGN.md §5)",
                 "fp64_pipe_frac": round(nb_pairs_s * FP64_OPS_PER_PAIR / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)}
@@ -393,7 +404,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=30.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

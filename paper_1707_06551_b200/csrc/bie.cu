@@ -182,11 +182,32 @@ static ChunkPlan plan_chunks(const bie_ctx* c, int64_t M, int64_t N, int occ) {
   if (c->chunks_override > 0) {
     S = c->chunks_override;
   } else {
+    // Units = target tiles x source chunks.  With many waves (>= 16 units per
+    // resident CTA slot) the hardware's dynamic CTA dispatch keeps the tail
+    // small; below that, pick the chunk count whose last wave is fullest.
     const int64_t slots = (int64_t)c->sm_count * std::max(occ, 1);
-    S = (64 * slots + P.n_tt - 1) / P.n_tt;  // ~64 units per CTA slot: small tail
-    S = std::min<int64_t>(S, std::max<int64_t>(1, n_src_tiles / 4));
     const int64_t cap = (int64_t)(kScratchBytes / (32.0 * std::max<int64_t>(M, 1)));
-    S = std::min<int64_t>(S, std::max<int64_t>(cap, 1));
+    int64_t smax = (64 * slots + P.n_tt - 1) / P.n_tt;  // ~64 units per CTA slot
+    smax = std::min<int64_t>(smax, std::max<int64_t>(1, n_src_tiles / 2));
+    smax = std::max<int64_t>(1, std::min<int64_t>(smax, cap));
+    if ((int64_t)P.n_tt * smax >= 16 * slots) {
+      S = smax;
+    } else {
+      S = 1;
+      double best = -1.0;
+      for (int64_t s = 1; s <= smax; ++s) {
+        const int64_t tpc = (n_src_tiles + s - 1) / s;
+        const int64_t se = (n_src_tiles + tpc - 1) / tpc;
+        const int64_t units = (int64_t)P.n_tt * se;
+        const int64_t waves = (units + slots - 1) / slots;
+        // busy fraction of the slot-time, with a per-unit start cost of ~1/20 tile
+        const double eff = (double)units / (double)(waves * slots) * (double)tpc / (tpc + 0.05);
+        if (eff > best + 1e-9) {
+          best = eff;
+          S = se;
+        }
+      }
+    }
   }
   S = std::max<int64_t>(1, std::min<int64_t>(S, n_src_tiles));
   P.tiles_per_chunk = (int)((n_src_tiles + S - 1) / S);
