@@ -48,6 +48,22 @@ def peak_fp64_tflops(mhz=SM_MAX_MHZ):
     return N_SM * FP64_LANES * 2 * mhz * 1e6 / 1e12
 
 
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of a per-rank float over all ranks (torch.distributed; identity at world 1)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(pairs_per_step: int, steps: int, world: int, max_total_ms: float) -> float:
+    """Whole-job throughput of N replicas: all ranks' pairs / max-over-ranks time."""
+    return world * pairs_per_step * steps / (max_total_ms / 1e3)
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
@@ -193,13 +209,9 @@ def run_gpu(args):
     clk = clocks.stop()
     prof = bie.bie_get_profile(ctx)
     bie.bie_set_profiling(ctx, False)
-    total_ms = float(sum(times))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(times), world, dev)
     ms_per_step = total_ms / args.steps
-    value = world * step_pairs * args.steps / (total_ms / 1e3)
+    value = replica_value(step_pairs, args.steps, world, total_ms)
     launches = int(sum(v[1] for k, v in prof.items() if k != "copy"))
 
     # dominant kernel: far-field pair sum of the apply (k_nbody)
@@ -270,12 +282,8 @@ def run_gpu(args):
             e1.record(stream)
             e1.synchronize()
             et.append(e0.elapsed_time(e1))
-        tot = float(sum(et))
-        if world > 1:
-            t = torch.tensor([tot], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            tot = float(t.item())
-        e2e = {"value": world * step_pairs * args.e2e_steps / (tot / 1e3), "unit": "pair-interactions/s",
+        tot = max_over_ranks(sum(et), world, dev)
+        e2e = {"value": replica_value(step_pairs, args.e2e_steps, world, tot), "unit": "pair-interactions/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": tot / args.e2e_steps}
 
