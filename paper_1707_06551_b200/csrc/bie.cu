@@ -253,7 +253,7 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   const size_t smem = self_smem_doubles(c->p) * sizeof(double);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
-  k_self<<<(unsigned)c->ns, 256, smem, s>>>(SA);
+  k_self<<<(unsigned)c->ns, 128, smem, s>>>(SA);
   prof_end(c, s, &ev);
   int rc = launch_check(c, "k_self");
   if (rc) return rc;

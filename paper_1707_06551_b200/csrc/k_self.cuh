@@ -7,11 +7,12 @@
 //   B  forward real DFT over the 2p+2 azimuthal nodes of every latitude
 //      (the FFT stage of the paper's fast transform; a dense
 //      26-point DFT at p = 12)
-//   C  Legendre projection per (n, m) (eq 2.3 discretised, reading R9) onto
-//      {Y e_r, G, X} (eq 2.12), conversion to {V, W, X} (eqs 2.13-2.14), and
-//      the diagonal scale psi = lamS (a/mu) alpha[f] + lamD_pv alpha[q]
-//      (Thm 2, readings R2/R3/R5/R6); back to {Y, G, X} (eqs 2.16-2.17)
-//   D  inverse Legendre sum per (latitude, m)
+//   C  Legendre projection per (density, n, m) (eq 2.3 discretised, reading
+//      R9) onto {Y e_r, G, X} (eq 2.12)
+//   C2 conversion to {V, W, X} (eqs 2.13-2.14), the diagonal scale
+//      psi = lamS (a/mu) alpha[f] + lamD_pv alpha[q] (Thm 2, readings
+//      R2/R3/R5/R6), back to {Y, G, X} (eqs 2.16-2.17)
+//   D  inverse Legendre sum per (component, latitude, m)
 //   E  inverse DFT, back to Cartesian, write u_self ("u may thus be
 //      evaluated using a fast inverse transform")
 // All intermediate spectra stay in shared memory; HBM sees f, q (48 B/node)
@@ -44,7 +45,7 @@ __host__ __device__ inline int64_t self_smem_doubles(int p) {
   return C + F + PSI + 2LL * nphi;
 }
 
-__global__ void __launch_bounds__(256) k_self(SelfArgs A) {
+__global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
   const TableLayout L(p);
@@ -52,8 +53,7 @@ __global__ void __launch_bounds__(256) k_self(SelfArgs A) {
   double* C = sm;                          // [2][3][nsn]
   double* F = C + 6 * nsn;                 // [2][3][P1][P1][2]
   double* PSI = F + 12 * P1 * P1;          // [nlm][3][2]
-  double* cs = PSI + 6 * nlm;              // cos(2 pi k/nphi)
-  double* sn = cs + nphi;                  // sin(2 pi k/nphi)
+  double2* tw = reinterpret_cast<double2*>(PSI + 6 * nlm);  // (cos, sin)(2 pi q/nphi)
   double* U = C;                           // [3][P1][P1][2] (C is dead after B)
   const double* __restrict__ tab = A.tab;
   const int64_t s = blockIdx.x;
@@ -63,10 +63,7 @@ __global__ void __launch_bounds__(256) k_self(SelfArgs A) {
   const double cS = 1.0 / (8.0 * kPi * A.mu), cD = 3.0 / (4.0 * kPi);
   const int tid = threadIdx.x, nt = blockDim.x;
 
-  for (int k = tid; k < nphi; k += nt) {
-    cs[k] = tab[L.cph + k];
-    sn[k] = tab[L.sph + k];
-  }
+  for (int k = tid; k < nphi; k += nt) tw[k] = make_double2(tab[L.cph + k], tab[L.sph + k]);
   // ---------------------------------------------------------------- A
   for (int kk = tid; kk < nsn; kk += nt) {
     const int j = kk / nphi, k = kk - j * nphi;
@@ -102,16 +99,31 @@ __global__ void __launch_bounds__(256) k_self(SelfArgs A) {
     return;
   }
   __syncthreads();
+  // ---------------------------------------------------------------- B0
+  // Real-signal symmetry of every latitude row g[k], k = 0..2p+1:
+  // in place, g[k] <- g[k] + g[nphi-k] and g[nphi-k] <- g[k] - g[nphi-k] for
+  // k = 1..p, so that the DFT below needs half the multiply-adds.
+  for (int it = tid; it < 6 * P1 * p; it += nt) {
+    const int row = it / p, k = 1 + it % p;
+    double* g = C + row * nphi;  // row = dc * P1 + j (C is [dc][j][k])
+    const double a0 = g[k], b0 = g[nphi - k];
+    g[k] = a0 + b0;
+    g[nphi - k] = a0 - b0;
+  }
+  __syncthreads();
   // ---------------------------------------------------------------- B
-  // F[dc][j][m] = sum_k C[dc][j,k] e^{-i m phi_k}
+  // F[dc][j][m] = sum_k g[k] e^{-i m phi_k}
+  //   = g0 + (-1)^m g_{p+1} + sum_{k=1}^{p} S_k cos(m phi_k) - i sum_k D_k sin(m phi_k)
   for (int it = tid; it < 6 * P1 * P1; it += nt) {
-    const int m = it % P1, j = (it / P1) % P1, dc = it / (P1 * P1);
-    const double* row = C + dc * nsn + j * nphi;
-    double re = 0.0, im = 0.0;
-    int idx = 0;
-    for (int k = 0; k < nphi; ++k) {
-      re = fma(row[k], cs[idx], re);
-      im = fma(-row[k], sn[idx], im);
+    const int m = it % P1, row = it / P1;
+    const double* g = C + row * nphi;
+    double re = (m & 1) ? g[0] - g[P1] : g[0] + g[P1];
+    double im = 0.0;
+    int idx = m;
+    for (int k = 1; k <= p; ++k) {
+      const double2 t = tw[idx];
+      re = fma(g[k], t.x, re);
+      im = fma(-g[nphi - k], t.y, im);
       idx += m;
       if (idx >= nphi) idx -= nphi;
     }
@@ -120,113 +132,139 @@ __global__ void __launch_bounds__(256) k_self(SelfArgs A) {
   }
   __syncthreads();
   // ---------------------------------------------------------------- C
-  for (int c = tid; c < nlm; c += nt) {
+  // Projection per (density, n, m): ALPHA[d][c] = (<F,Y e_r>, <F,G>, <F,X>),
+  // complex.  ALPHA aliases C, which is dead after phase B.
+  double* ALPHA = C;  // [2][nlm][3][2]
+  for (int it = tid; it < 2 * nlm; it += nt) {
+    const int d = it / nlm, c = it - d * nlm;
     int m = 0, off = 0;
     while (off + (P1 - m) <= c) { off += P1 - m; ++m; }
-    const int n = m + (c - off);
-    double acc[2][3][2];  // [dens][Y,<G>,<X>][re,im]
-#pragma unroll
-    for (int d = 0; d < 2; ++d)
-#pragma unroll
-      for (int z = 0; z < 3; ++z) acc[d][z][0] = acc[d][z][1] = 0.0;
+    double y0 = 0, y1 = 0, g0 = 0, g1 = 0, x0 = 0, x1 = 0;
     for (int j = 0; j < P1; ++j) {
       const double wj = tab[L.wu + j];
       const double Pv = wj * tab[L.P + (int64_t)j * nlm + c];
       const double dPv = wj * tab[L.dP + (int64_t)j * nlm + c];
       const double mPv = wj * tab[L.mPs + (int64_t)j * nlm + c];
-#pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        const double* Fr = F + 2 * (((3 * d + 0) * P1 + j) * P1 + m);
-        const double* Ft = F + 2 * (((3 * d + 1) * P1 + j) * P1 + m);
-        const double* Fp = F + 2 * (((3 * d + 2) * P1 + j) * P1 + m);
-        // <F, Y e_r>
-        acc[d][0][0] = fma(Pv, Fr[0], acc[d][0][0]);
-        acc[d][0][1] = fma(Pv, Fr[1], acc[d][0][1]);
-        // <F, G> = dP F_t - i mP F_p
-        acc[d][1][0] = fma(dPv, Ft[0], fma(mPv, Fp[1], acc[d][1][0]));
-        acc[d][1][1] = fma(dPv, Ft[1], fma(-mPv, Fp[0], acc[d][1][1]));
-        // <F, X> = dP F_p + i mP F_t
-        acc[d][2][0] = fma(dPv, Fp[0], fma(-mPv, Ft[1], acc[d][2][0]));
-        acc[d][2][1] = fma(dPv, Fp[1], fma(mPv, Ft[0], acc[d][2][1]));
-      }
+      const double* Fr = F + 2 * (((3 * d + 0) * P1 + j) * P1 + m);
+      const double* Ft = F + 2 * (((3 * d + 1) * P1 + j) * P1 + m);
+      const double* Fp = F + 2 * (((3 * d + 2) * P1 + j) * P1 + m);
+      y0 = fma(Pv, Fr[0], y0);                        // <F, Y e_r>
+      y1 = fma(Pv, Fr[1], y1);
+      g0 = fma(dPv, Ft[0], fma(mPv, Fp[1], g0));      // <F, G> = dP F_t - i mP F_p
+      g1 = fma(dPv, Ft[1], fma(-mPv, Fp[0], g1));
+      x0 = fma(dPv, Fp[0], fma(-mPv, Ft[1], x0));     // <F, X> = dP F_p + i mP F_t
+      x1 = fma(dPv, Fp[1], fma(mPv, Ft[0], x1));
     }
+    double* o = ALPHA + 6 * it;
+    o[0] = y0; o[1] = y1; o[2] = g0; o[3] = g1; o[4] = x0; o[5] = x1;
+  }
+  __syncthreads();
+  // ---------------------------------------------------------------- C2
+  // {Y,G,X} -> {V,W,X} (eqs 2.13-2.14), diagonal scale (Thm 2), back to
+  // {Y,G,X} (eqs 2.16-2.17) for the inverse transform.
+  for (int c = tid; c < nlm; c += nt) {
+    int m = 0, off = 0;
+    while (off + (P1 - m) <= c) { off += P1 - m; ++m; }
+    const int n = m + (c - off);
     const double* lS = tab + L.lamS + 3 * n;
     const double* lD = tab + L.lamD + 3 * n;
     const double inn = n ? 1.0 / ((double)n * (n + 1)) : 0.0;
     const double i2n = 1.0 / (2.0 * n + 1.0);
-    double psV[2], psW[2], psX[2];
+    const double* af = ALPHA + 6 * c;
+    const double* aq = ALPHA + 6 * (nlm + c);
+    double* o = PSI + 6 * c;
 #pragma unroll
     for (int ri = 0; ri < 2; ++ri) {
       double aV[2], aW[2], aX[2];
+      const double* al[2] = {af, aq};
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        const double phY = acc[d][0][ri], phG = acc[d][1][ri] * inn, phX = acc[d][2][ri] * inn;
+        const double phY = al[d][ri], phG = al[d][2 + ri] * inn, phX = al[d][4 + ri] * inn;
         aV[d] = (n * phG - phY) * i2n;          // eq 2.13
         aW[d] = ((n + 1) * phG + phY) * i2n;    // eq 2.14
         aX[d] = phX;
       }
-      psV[ri] = lS[0] * aV[0] + lD[0] * aV[1];
-      psW[ri] = lS[1] * aW[0] + lD[1] * aW[1];
-      psX[ri] = lS[2] * aX[0] + lD[2] * aX[1];
-    }
-    double* o = PSI + 6 * c;
-#pragma unroll
-    for (int ri = 0; ri < 2; ++ri) {
-      o[0 + ri] = -(n + 1.0) * psV[ri] + n * psW[ri];  // psi^Y (eq 2.17)
-      o[2 + ri] = psV[ri] + psW[ri];                   // psi^G (eq 2.16)
-      o[4 + ri] = psX[ri];                             // psi^X
+      const double psV = lS[0] * aV[0] + lD[0] * aV[1];
+      const double psW = lS[1] * aW[0] + lD[1] * aW[1];
+      const double psX = lS[2] * aX[0] + lD[2] * aX[1];
+      o[0 + ri] = -(n + 1.0) * psV + n * psW;  // psi^Y (eq 2.17)
+      o[2 + ri] = psV + psW;                   // psi^G (eq 2.16)
+      o[4 + ri] = psX;                         // psi^X
     }
   }
   __syncthreads();
   // ---------------------------------------------------------------- D
+  // one (component, latitude, m) per item:
   // U_r = sum_n psiY P, U_t = sum_n psiG dP - i psiX mP, U_p = sum_n i psiG mP + psiX dP
-  for (int it = tid; it < P1 * P1; it += nt) {
-    const int j = it / P1, m = it % P1;
-    double ur0 = 0, ur1 = 0, ut0 = 0, ut1 = 0, up0 = 0, up1 = 0;
+  for (int it = tid; it < 3 * P1 * P1; it += nt) {
+    const int comp = it / (P1 * P1);
+    const int j = (it / P1) % P1, m = it % P1;
+    double a0 = 0, a1 = 0;
     const int c0 = lm_index(p, m, m);
-    for (int n = m; n <= p; ++n) {
-      const int c = c0 + (n - m);
-      const double Pv = tab[L.P + (int64_t)j * nlm + c];
-      const double dPv = tab[L.dP + (int64_t)j * nlm + c];
-      const double mPv = tab[L.mPs + (int64_t)j * nlm + c];
-      const double* ps = PSI + 6 * c;
-      ur0 = fma(ps[0], Pv, ur0);
-      ur1 = fma(ps[1], Pv, ur1);
-      ut0 = fma(ps[2], dPv, fma(ps[5], mPv, ut0));
-      ut1 = fma(ps[3], dPv, fma(-ps[4], mPv, ut1));
-      up0 = fma(ps[4], dPv, fma(-ps[3], mPv, up0));
-      up1 = fma(ps[5], dPv, fma(ps[2], mPv, up1));
+    const double* Pj = tab + L.P + (int64_t)j * nlm;
+    const double* dPj = tab + L.dP + (int64_t)j * nlm;
+    const double* mPj = tab + L.mPs + (int64_t)j * nlm;
+    if (comp == 0) {
+      for (int c = c0; c < c0 + (P1 - m); ++c) {
+        const double* ps = PSI + 6 * c;
+        a0 = fma(ps[0], Pj[c], a0);
+        a1 = fma(ps[1], Pj[c], a1);
+      }
+    } else if (comp == 1) {
+      for (int c = c0; c < c0 + (P1 - m); ++c) {
+        const double* ps = PSI + 6 * c;
+        a0 = fma(ps[2], dPj[c], fma(ps[5], mPj[c], a0));
+        a1 = fma(ps[3], dPj[c], fma(-ps[4], mPj[c], a1));
+      }
+    } else {
+      for (int c = c0; c < c0 + (P1 - m); ++c) {
+        const double* ps = PSI + 6 * c;
+        a0 = fma(ps[4], dPj[c], fma(-ps[3], mPj[c], a0));
+        a1 = fma(ps[5], dPj[c], fma(ps[2], mPj[c], a1));
+      }
     }
-    U[2 * ((0 * P1 + j) * P1 + m)] = ur0;
-    U[2 * ((0 * P1 + j) * P1 + m) + 1] = ur1;
-    U[2 * ((1 * P1 + j) * P1 + m)] = ut0;
-    U[2 * ((1 * P1 + j) * P1 + m) + 1] = ut1;
-    U[2 * ((2 * P1 + j) * P1 + m)] = up0;
-    U[2 * ((2 * P1 + j) * P1 + m) + 1] = up1;
+    U[2 * it] = a0;
+    U[2 * it + 1] = a1;
   }
   __syncthreads();
   // ---------------------------------------------------------------- E
-  for (int kk = tid; kk < nsn; kk += nt) {
-    const int j = kk / nphi, k = kk - j * nphi;
-    double v[3];
+  // Inverse DFT for the node pair (k, nphi-k) of a latitude:
+  //   u(k) = U0 + 2(c - s), u(nphi-k) = U0 + 2(c + s),
+  //   c = sum_m Re U_m cos(m phi_k), s = sum_m Im U_m sin(m phi_k),
+  // then spherical -> Cartesian components and the store of u_self.
+  for (int it = tid; it < P1 * (P1 + 1); it += nt) {
+    const int j = it / (P1 + 1), k = it % (P1 + 1);
+    double c[3] = {0, 0, 0}, sn_[3] = {0, 0, 0};
+    int idx = k;
+    for (int m = 1; m <= p; ++m) {
+      const double2 t = tw[idx];
 #pragma unroll
-    for (int comp = 0; comp < 3; ++comp) {
-      const double* Uc = U + 2 * ((comp * P1 + j) * P1);
-      double acc = 0.0;
-      int idx = k;
-      for (int m = 1; m <= p; ++m) {
-        acc = fma(Uc[2 * m], cs[idx], fma(-Uc[2 * m + 1], sn[idx], acc));
-        idx += k;
-        if (idx >= nphi) idx -= nphi;
+      for (int comp = 0; comp < 3; ++comp) {
+        const double2 Um = reinterpret_cast<const double2*>(U)[(comp * P1 + j) * P1 + m];
+        c[comp] = fma(Um.x, t.x, c[comp]);
+        sn_[comp] = fma(Um.y, t.y, sn_[comp]);
       }
-      v[comp] = fma(2.0, acc, Uc[0]);
+      idx += k;
+      if (idx >= nphi) idx -= nphi;
     }
     const double ct = tab[L.t + j], st = tab[L.st + j];
-    const double cp = cs[k], sp = sn[k];
-    const int64_t i = s * nsn + kk;
-    A.u[3 * i + 0] = v[0] * st * cp + v[1] * ct * cp - v[2] * sp;
-    A.u[3 * i + 1] = v[0] * st * sp + v[1] * ct * sp + v[2] * cp;
-    A.u[3 * i + 2] = v[0] * ct - v[1] * st;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      if (side == 1 && (k == 0 || k == P1)) break;
+      const int kk = side ? nphi - k : k;
+      double v[3];
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp) {
+        const double U0 = U[2 * ((comp * P1 + j) * P1)];
+        v[comp] = fma(2.0, side ? c[comp] + sn_[comp] : c[comp] - sn_[comp], U0);
+      }
+      const double2 t = tw[kk];
+      const double cp = t.x, sp = t.y;
+      const int64_t i = s * nsn + j * nphi + kk;
+      A.u[3 * i + 0] = v[0] * st * cp + v[1] * ct * cp - v[2] * sp;
+      A.u[3 * i + 1] = v[0] * st * sp + v[1] * ct * sp + v[2] * cp;
+      A.u[3 * i + 2] = v[0] * ct - v[1] * st;
+    }
   }
 }
 
