@@ -182,3 +182,54 @@ def eigen(n, ch):
     v = [ctypes.c_double() for _ in range(4)]
     _load().oracle_eigen(n, ch, *[ctypes.byref(x) for x in v])
     return tuple(x.value for x in v)
+
+
+# ---------------------------------------------------------------- NEXT-1
+def _load_near():
+    lib = _load()
+    if not getattr(lib, "_near_ready", False):
+        i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        lib.oracle_exterior_eval.argtypes = [i32, _DP, d, d, _DP, _DP, _DP, i64, _DP]
+        lib.oracle_is_near.argtypes = [_DP, d, _DP, d, d]
+        lib.oracle_near.argtypes = [_DP, _DP, i64, i32, d, _DP, _DP, d, _I64P, i64, _DP]
+        lib._near_ready = True
+    return lib
+
+
+def exterior_eval(p, centre, a, mu, f_s, q_s, targets):
+    """Exact exterior S[f_s] + D[q_s] of ONE sphere from its degree-<=p VSH
+    expansion (eqs 3.6-3.11; eq 4.7) at targets [M,3]."""
+    lib = _load_near()
+    c = _c(np.asarray(centre, dtype=np.float64).reshape(3))
+    f_s, q_s, targets = _c(f_s), _c(q_s), _c(targets)
+    M = targets.shape[0]
+    u = np.empty((M, 3))
+    if lib.oracle_exterior_eval(p, _dp(c), a, mu, _dp(f_s), _dp(q_s), _dp(targets), M, _dp(u)):
+        raise ValueError("exterior_eval: bad arguments")
+    return u
+
+
+def is_near(cs, a_s, ct, a_t, eta):
+    """eq 4.5: True if the two spheres are NOT well separated."""
+    lib = _load_near()
+    cs = _c(np.asarray(cs, dtype=np.float64).reshape(3))
+    ct = _c(np.asarray(ct, dtype=np.float64).reshape(3))
+    return bool(lib.oracle_is_near(_dp(cs), a_s, _dp(ct), a_t, eta))
+
+
+def near(centres, radii, p, mu, f, q, eta, subset=None):
+    """Near-singular correction du (exact minus smooth) at nodes `subset`."""
+    lib = _load_near()
+    centres, radii, f, q = _c(centres), _c(radii), _c(f), _c(q)
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    idx = _subset(subset, N)
+    du = np.empty((len(idx), 3))
+    if lib.oracle_near(_dp(centres), _dp(radii), len(radii), p, mu, _dp(f), _dp(q), eta,
+                       idx.ctypes.data_as(_I64P), len(idx), _dp(du)):
+        raise ValueError("near: bad arguments")
+    return du
+
+
+def apply_near(centres, radii, p, mu, f, q, eta, subset=None):
+    """Composite apply with the near-singular correction: far + self + near."""
+    return apply(centres, radii, p, mu, f, q, subset) + near(centres, radii, p, mu, f, q, eta, subset)

@@ -499,3 +499,173 @@ extern "C" int oracle_self_addthm(int p, double mu, double a, const double* f, c
 
 extern "C" int oracle_num_threads(void) { return omp_get_max_threads(); }
 extern "C" void oracle_set_num_threads(int n) { if (n > 0) omp_set_num_threads(n); }
+
+// ============================================================ NEXT-1 (near)
+// Near-singular correction (PAPER §4.1 "Singular and near-singular
+// integrands"; composite scheme §4.3).  Sphere pairs that
+// fail the well-separation test of eq 4.5,
+//     dist(G_src, G_trg) >= eta max(diam(G_src), diam(G_trg)),
+// with dist = |c_s - c_t| - a_s - a_t and diam = 2a, are not evaluated with
+// the smooth rule: the source density is expanded in VSH of degree <= p
+// (eq 4.6, the discrete projection of reading R9) and the exterior formulas
+// of eqs 3.6-3.11 (sign reading R1) are evaluated at the targets (eq 4.7).
+
+// VSH coefficients of one sphere: alpha[(n*n+n+m)*3 + ch] for the density
+// g_k (node order of the sphere), alpha = (1/||Z_n||^2) sum_k w^_k g_k . conj Z.
+static void project_sphere(int p, const double* g, std::vector<cplx>& alpha) {
+  const int nphi = 2 * p + 2, nsn = (p + 1) * nphi, nlm = (p + 1) * (p + 1);
+  std::vector<double> t(p + 1), lam(p + 1);
+  oracle_gl_rule(p, t.data(), lam.data());
+  alpha.assign((size_t)nlm * 3, cplx(0.0, 0.0));
+  for (int j = 0; j <= p; ++j)
+    for (int k = 0; k < nphi; ++k) {
+      const int kk = j * nphi + k;
+      const double wk = lam[j] * 2.0 * PI / nphi;
+      const double th = std::acos(t[j]), ph = 2.0 * PI * k / nphi;
+      for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m) {
+          cplx z[9];
+          vsh_cart(n, m, th, ph, z);
+          for (int ch = 0; ch < 3; ++ch) {
+            if (n == 0 && ch > 0) continue;
+            cplx acc(0.0, 0.0);
+            for (int c = 0; c < 3; ++c) acc += g[3 * kk + c] * std::conj(z[3 * ch + c]);
+            alpha[(size_t)(n * n + n + m) * 3 + ch] += wk * acc;
+          }
+        }
+    }
+  for (int n = 0; n <= p; ++n)
+    for (int m = -n; m <= n; ++m)
+      for (int ch = 0; ch < 3; ++ch) alpha[(size_t)(n * n + n + m) * 3 + ch] /= (n == 0 && ch > 0) ? 1.0 : vsh_norm2(n, ch);
+  (void)nsn;
+}
+
+// Exterior field (r >= 1, unit sphere) of a unit-coefficient density Z_n^m,
+// channel ch, for S (kind 0) or D (kind 1): eqs 3.6-3.8 / 3.9-3.11.
+// Zv, Zw, Zx: V_n^m, W_n^m, X_n^m at the target's angles (complex Cartesian).
+static void exterior_unit(int kind, int ch, int n, double r, const cplx* Zv, const cplx* Zw,
+                          const cplx* Zx, cplx out[3]) {
+  const double a = 2.0 * n + 1.0;
+  for (int c = 0; c < 3; ++c) out[c] = 0.0;
+  if (kind == 0) {
+    if (ch == 0) {
+      for (int c = 0; c < 3; ++c) out[c] = n / (a * (2.0 * n + 3.0)) * Zv[c] * std::pow(r, -n - 2.0);
+    } else if (ch == 1) {
+      for (int c = 0; c < 3; ++c)
+        out[c] = (n + 1.0) / (a * (2.0 * n - 1.0)) * Zw[c] * std::pow(r, -(double)n) +
+                 n / (4.0 * n + 2.0) * Zv[c] * (std::pow(r, -n - 2.0) - std::pow(r, -(double)n));
+    } else {
+      for (int c = 0; c < 3; ++c) out[c] = 1.0 / a * Zx[c] * std::pow(r, -n - 1.0);
+    }
+  } else {
+    if (ch == 0) {
+      for (int c = 0; c < 3; ++c)
+        out[c] = (2.0 * n * n + 4.0 * n + 3.0) / (a * (2.0 * n + 3.0)) * Zv[c] * std::pow(r, -n - 2.0);
+    } else if (ch == 1) {
+      for (int c = 0; c < 3; ++c)
+        out[c] = 2.0 * (n + 1.0) * (n - 1.0) / (a * (2.0 * n - 1.0)) * Zw[c] * std::pow(r, -(double)n) +
+                 2.0 * n * (n - 1.0) / (4.0 * n + 2.0) * Zv[c] * (std::pow(r, -n - 2.0) - std::pow(r, -(double)n));
+    } else {
+      for (int c = 0; c < 3; ++c) out[c] = (n - 1.0) / a * Zx[c] * std::pow(r, -n - 1.0);
+    }
+  }
+}
+
+// Field of sphere (c, a) carrying densities f (S) and q (D) [nsn][3] at an
+// exterior point x: u = sum_{n<=p,m,Z} (a/mu) alpha_Z[f] S[Z](r) + alpha_Z[q] D[Z](r)
+// with r = |x - c|/a (radius/viscosity scalings R5, R6).
+static void exterior_eval(int p, const double* c, double a, double mu,
+                          const std::vector<cplx>* af, const std::vector<cplx>* aq,
+                          const double* x, double u[3]) {
+  const double rv[3] = {(x[0] - c[0]) / a, (x[1] - c[1]) / a, (x[2] - c[2]) / a};
+  const double r = std::sqrt(rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2]);
+  const double th = std::acos(rv[2] / r), ph = std::atan2(rv[1], rv[0]);
+  cplx acc[3] = {0.0, 0.0, 0.0};
+  for (int n = 0; n <= p; ++n)
+    for (int m = -n; m <= n; ++m) {
+      cplx z[9];
+      vsh_cart(n, m, th, ph, z);
+      for (int ch = 0; ch < 3; ++ch) {
+        if (n == 0 && ch > 0) continue;
+        const size_t ix = (size_t)(n * n + n + m) * 3 + ch;
+        cplx e[3];
+        if (af) {
+          exterior_unit(0, ch, n, r, z, z + 3, z + 6, e);
+          for (int k = 0; k < 3; ++k) acc[k] += (a / mu) * (*af)[ix] * e[k];
+        }
+        if (aq) {
+          exterior_unit(1, ch, n, r, z, z + 3, z + 6, e);
+          for (int k = 0; k < 3; ++k) acc[k] += (*aq)[ix] * e[k];
+        }
+      }
+    }
+  for (int k = 0; k < 3; ++k) u[k] = acc[k].real();
+}
+
+// Velocity of the spectral (exact) layer potentials of ONE sphere at m
+// exterior targets: f_s, q_s are that sphere's nodal densities [nsn][3] (either
+// may be NULL).  Used by the near correction and pinned on its own.
+extern "C" int oracle_exterior_eval(int p, const double* c, double a, double mu, const double* f_s,
+                                    const double* q_s, const double* targets, int64_t m, double* u) {
+  if (p < 1 || !(a > 0) || !(mu > 0) || !c || (m > 0 && (!targets || !u))) return 1;
+  std::vector<cplx> af, aq;
+  if (f_s) project_sphere(p, f_s, af);
+  if (q_s) project_sphere(p, q_s, aq);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < m; ++t)
+    exterior_eval(p, c, a, mu, f_s ? &af : nullptr, q_s ? &aq : nullptr, targets + 3 * t, u + 3 * t);
+  return 0;
+}
+
+// eq 4.5: true when spheres s and t are NOT well separated (and s != t).
+extern "C" int oracle_is_near(const double* cs, double as, const double* ct, double at, double eta) {
+  const double d = std::sqrt((cs[0] - ct[0]) * (cs[0] - ct[0]) + (cs[1] - ct[1]) * (cs[1] - ct[1]) +
+                             (cs[2] - ct[2]) * (cs[2] - ct[2])) - as - at;
+  return d < eta * std::max(2.0 * as, 2.0 * at) ? 1 : 0;
+}
+
+// Near correction at the subset nodes tidx: du_i = sum over near spheres s of
+// [ exterior_eval of sphere s at x_i  -  smooth-rule sum over s's nodes at x_i ].
+// The corrected apply is oracle_far + oracle_self + oracle_near.
+extern "C" int oracle_near(const double* centres, const double* radii, int64_t ns, int p, double mu,
+                           const double* f, const double* q, double eta, const int64_t* tidx,
+                           int64_t nt, double* du) {
+  if (ns < 1 || p < 1 || !(mu > 0) || !(eta >= 0) || !du || !tidx) return 1;
+  Geometry G(centres, radii, ns, p);
+  const int nsn = G.nsn;
+  // spheres whose expansion is needed
+  std::vector<char> need(ns, 0);
+  for (int64_t a = 0; a < nt; ++a) {
+    const int64_t t = tidx[a] / nsn;
+    for (int64_t s = 0; s < ns; ++s)
+      if (s != t && oracle_is_near(centres + 3 * s, radii[s], centres + 3 * t, radii[t], eta)) need[s] = 1;
+  }
+  std::vector<std::vector<cplx>> AF(ns), AQ(ns);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = 0; s < ns; ++s) {
+    if (!need[s]) continue;
+    if (f) project_sphere(p, f + 3 * s * nsn, AF[s]);
+    if (q) project_sphere(p, q + 3 * s * nsn, AQ[s]);
+  }
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t a = 0; a < nt; ++a) {
+    const int64_t i = tidx[a], t = i / nsn;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t s = 0; s < ns; ++s) {
+      if (s == t || !oracle_is_near(centres + 3 * s, radii[s], centres + 3 * t, radii[t], eta)) continue;
+      double ue[3];
+      exterior_eval(p, centres + 3 * s, radii[s], mu, f ? &AF[s] : nullptr, q ? &AQ[s] : nullptr,
+                    &G.x[3 * i], ue);
+      Neumaier sm[3];
+      for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
+        double v[3];
+        pair_terms(&G.x[3 * i], &G.x[3 * k], &G.n[3 * k], G.w[k], f ? f + 3 * k : nullptr,
+                   q ? q + 3 * k : nullptr, mu, v, nullptr);
+        for (int c = 0; c < 3; ++c) sm[c].add(v[c]);
+      }
+      for (int c = 0; c < 3; ++c) acc[c] += ue[c] - sm[c].get();
+    }
+    for (int c = 0; c < 3; ++c) du[3 * a + c] = acc[c];
+  }
+  return 0;
+}
