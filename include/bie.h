@@ -62,7 +62,8 @@ enum bie_status {
 #define BIE_KIND_REDUCE 4   /* deterministic reduction of source-chunk partials */
 #define BIE_KIND_OFFSURF 5  /* off-surface u,p pair sum (a7)                    */
 #define BIE_KIND_COPY 6     /* host<->device copies of the _host entry points   */
-#define BIE_NUM_KINDS 7
+#define BIE_KIND_NEAR 7     /* near-singular correction (NEXT-1)              */
+#define BIE_NUM_KINDS 8
 
 /*
  * bie_create -- build nodes, weights, normals and spectral tables (row a1).
@@ -164,6 +165,24 @@ int bie_eval_offsurface_host(bie_ctx* ctx, const double* f_h, const double* q_h,
 int bie_set_profiling(bie_ctx* ctx, int enable);
 int bie_get_profile(bie_ctx* ctx, double* ms, int64_t* launches);
 int bie_reset_profile(bie_ctx* ctx);
+
+/*
+ * bie_set_near -- near-singular correction (PAPER §4.1 "Singular and
+ * near-singular integrands"; §4.3).  eta > 0 enables it:
+ * every sphere pair that is not well separated by eq 4.5,
+ *     |c_s - c_t| - a_s - a_t  <  eta * max(2 a_s, 2 a_t),
+ * has its smooth-rule contribution in bie_apply_* replaced by the exact
+ * exterior field of the source sphere's degree-<=p vector spherical harmonic
+ * expansion (eqs 3.6-3.11 with reading R1, eq 4.7; the expansion is the
+ * discrete projection of reading R9).  eta = 0 disables it (the default, and
+ * the BASELINE.json metric path).  Builds the neighbour lists on the device
+ * and synchronises.  BIE_ERR_ARG for eta < 0 or non-finite.
+ * The off-surface evaluator is not affected.
+ */
+int bie_set_near(bie_ctx* ctx, double eta);
+
+/* Number of (target sphere, source sphere) near pairs of the current eta; -1 for NULL. */
+int64_t bie_near_pairs(const bie_ctx* ctx);
 
 /*
  * Tuning knob: number of source chunks of the far-field kernel (0 = automatic;

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libbie.so")
 BIE_OK, BIE_ERR_ARG, BIE_ERR_GEOMETRY, BIE_ERR_ALLOC, BIE_ERR_CUDA, BIE_ERR_UNSUPPORTED = range(6)
 BIE_P_MAX = 30
 BIE_PART_FAR, BIE_PART_SELF = 1, 2
-KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy")
+KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near")
 BIE_NUM_KINDS = len(KINDS)
 
 #: every symbol include/bie.h declares (checked by tests/test_abi_cpu.py)
@@ -22,6 +22,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
+    "bie_set_near", "bie_near_pairs",
     "bie_status_string", "bie_last_error",
 )
 
@@ -52,6 +53,9 @@ _lib.bie_set_profiling.argtypes = [_vp, _i32]
 _lib.bie_get_profile.argtypes = [_vp, _DP, ctypes.POINTER(_i64)]
 _lib.bie_reset_profile.argtypes = [_vp]
 _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
+_lib.bie_set_near.argtypes = [_vp, _d]
+_lib.bie_near_pairs.argtypes = [_vp]
+_lib.bie_near_pairs.restype = _i64
 _lib.bie_status_string.argtypes = [_i32]
 _lib.bie_status_string.restype = ctypes.c_char_p
 _lib.bie_last_error.argtypes = [_vp]
@@ -243,6 +247,15 @@ def bie_reset_profile(ctx):
 
 def bie_set_source_chunks(ctx, chunks: int):
     _check(ctx, _lib.bie_set_source_chunks(ctx.handle, int(chunks)))
+
+
+def bie_set_near(ctx, eta: float):
+    """Enable (eta > 0) or disable (eta = 0) the near-singular correction."""
+    _check(ctx, _lib.bie_set_near(ctx.handle, float(eta)))
+
+
+def bie_near_pairs(ctx) -> int:
+    return int(_lib.bie_near_pairs(ctx.handle))
 
 
 def bie_status_string(status: int) -> str:

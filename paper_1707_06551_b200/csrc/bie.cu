@@ -13,6 +13,7 @@
 #include "../../include/bie.h"
 #include "common.cuh"
 #include "k_nbody.cuh"
+#include "k_near.cuh"
 #include "k_self.cuh"
 #include "k_setup.cuh"
 
@@ -55,6 +56,14 @@ struct bie_ctx {
   double* d_part = nullptr;
   size_t part_cap = 0;  // doubles
   int chunks_override = 0;
+  // near-singular correction (NEXT-1)
+  double eta = 0.0;
+  int n_near_tgt = 0;
+  int64_t n_near_pairs = 0;
+  int* d_nb_off = nullptr;
+  int* d_nb_idx = nullptr;
+  int* d_near_tgt = nullptr;
+  double* d_alpha = nullptr;
   // staging for the _host entry points
   double *d_f = nullptr, *d_q = nullptr, *d_u = nullptr;
   double *d_tg = nullptr, *d_uo = nullptr, *d_po = nullptr;
@@ -235,6 +244,8 @@ static int launch_check(bie_ctx* c, const char* what) {
   return BIE_OK;
 }
 
+static int run_far(bie_ctx* c, double* u, cudaStream_t s);
+
 static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
                      cudaStream_t s) {
   // rows a2 + a4-a6: self term (or zeros) into u, packed sources into d_rec
@@ -250,6 +261,8 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   SA.u = u;
   SA.rec = c->d_rec;
   SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
+  const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
+  SA.alpha = near ? c->d_alpha : nullptr;
   const size_t smem = self_smem_doubles(c->p) * sizeof(double);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
@@ -258,7 +271,32 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   int rc = launch_check(c, "k_self");
   if (rc) return rc;
   if (!(parts & BIE_PART_FAR)) return BIE_OK;
-  // row a3: far field
+  rc = run_far(c, u, s);
+  if (rc || !near) return rc;
+  // NEXT-1: replace the smooth rule by the exterior expansion for near pairs
+  NearArgs NA;
+  NA.p = c->p;
+  NA.nsn = c->nsn;
+  NA.mu = c->mu;
+  NA.tab = c->d_tab;
+  NA.centres = c->d_centres;
+  NA.radii = c->d_radii;
+  NA.rec = c->d_rec;
+  NA.alpha = c->d_alpha;
+  NA.tgt = c->d_near_tgt;
+  NA.nb_off = c->d_nb_off;
+  NA.nb_idx = c->d_nb_idx;
+  NA.u = u;
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  k_near<<<(unsigned)c->n_near_tgt, 128, near_smem_doubles(c->p) * sizeof(double), s>>>(NA);
+  prof_end(c, s, &ev);
+  return launch_check(c, "k_near");
+}
+
+// row a3: far-field smooth sum over all other spheres, accumulated onto u
+static int run_far(bie_ctx* c, double* u, cudaStream_t s) {
+  Ev ev;
+  int rc;
   const ChunkPlan P = plan_chunks(c, c->N, c->N, c->occ_apply);
   NbodyArgs A;
   A.rec = c->d_rec;
@@ -376,6 +414,10 @@ void bie_destroy(bie_ctx* c) {
                     c->d_qn3, c->d_part, c->d_f, c->d_q, c->d_u, c->d_tg, c->d_uo, c->d_po};
   for (double* p : ptrs)
     if (p) cudaFree(p);
+  int* iptrs[] = {c->d_nb_off, c->d_nb_idx, c->d_near_tgt};
+  for (int* p : iptrs)
+    if (p) cudaFree(p);
+  if (c->d_alpha) cudaFree(c->d_alpha);
   delete c;
 }
 
@@ -441,6 +483,8 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   prof_end(c, 0, &ev);
   const size_t smem = self_smem_doubles(p) * sizeof(double);
   cudaFuncSetAttribute(k_self, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_near, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_smem_doubles(p) * sizeof(double)));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
@@ -630,6 +674,66 @@ int bie_reset_profile(bie_ctx* c) {
   }
   return BIE_OK;
 }
+
+static void near_free(bie_ctx* c) {
+  cudaFree(c->d_nb_off);
+  cudaFree(c->d_nb_idx);
+  cudaFree(c->d_near_tgt);
+  cudaFree(c->d_alpha);
+  c->d_nb_off = c->d_nb_idx = c->d_near_tgt = nullptr;
+  c->d_alpha = nullptr;
+  c->n_near_tgt = 0;
+  c->n_near_pairs = 0;
+}
+
+int bie_set_near(bie_ctx* c, double eta) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (!(eta >= 0.0) || !std::isfinite(eta)) return fail(c, BIE_ERR_ARG, "eta must be finite and >= 0%s");
+  cudaDeviceSynchronize();
+  near_free(c);
+  c->eta = eta;
+  if (eta == 0.0) return BIE_OK;
+  const int64_t ns = c->ns;
+  int* d_cnt = nullptr;
+  if (cudaMalloc(&d_cnt, ns * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->d_nb_off, (ns + 1) * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(d_cnt);
+    near_free(c);
+    return fail(c, BIE_ERR_ALLOC, "near lists%s");
+  }
+  const unsigned g = (unsigned)((ns + 127) / 128);
+  k_near_lists<<<g, 128>>>(ns, c->d_centres, c->d_radii, eta, d_cnt, nullptr, nullptr);
+  std::vector<int> cnt(ns), off(ns + 1, 0), tgt;
+  cudaMemcpy(cnt.data(), d_cnt, ns * sizeof(int), cudaMemcpyDeviceToHost);
+  for (int64_t t = 0; t < ns; ++t) {
+    off[t + 1] = off[t] + cnt[t];
+    if (cnt[t]) tgt.push_back((int)t);
+  }
+  c->n_near_pairs = off[ns];
+  c->n_near_tgt = (int)tgt.size();
+  cudaFree(d_cnt);
+  if (c->n_near_pairs == 0) return launch_check(c, "k_near_lists");
+  const TableLayout L(c->p);
+  if (cudaMalloc(&c->d_nb_idx, off[ns] * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->d_near_tgt, tgt.size() * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->d_alpha, (size_t)ns * 12 * L.nlm * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    near_free(c);
+    return fail(c, BIE_ERR_ALLOC, "near lists%s");
+  }
+  cudaMemcpy(c->d_nb_off, off.data(), (ns + 1) * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->d_near_tgt, tgt.data(), tgt.size() * sizeof(int), cudaMemcpyHostToDevice);
+  k_near_lists<<<g, 128>>>(ns, c->d_centres, c->d_radii, eta, nullptr, c->d_nb_off, c->d_nb_idx);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, "bie_set_near");
+  return BIE_OK;
+}
+
+int64_t bie_near_pairs(const bie_ctx* c) { return c ? c->n_near_pairs : -1; }
 
 int bie_set_source_chunks(bie_ctx* c, int chunks) {
   if (!c) return BIE_ERR_ARG;

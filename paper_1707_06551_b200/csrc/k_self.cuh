@@ -35,6 +35,8 @@ struct SelfArgs {
   double* u;        // [N][3] out: self term (or 0 when !self)
   double* rec;      // [N][kRec] out: packed sources
   int self;         // compute the self term (else write zeros)
+  double* alpha;    // nullable: [ns][2][nlm][3][2] projections <F,Y e_r>, <F,G>, <F,X>
+                    // of (a/mu) f and q, for the near-singular correction (k_near)
 };
 
 __host__ __device__ inline int64_t self_smem_doubles(int p) {
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
     r2[3] = make_double2(ws * f0, ws * f1);
     r2[4] = make_double2(ws * f2, wd * q0);
     r2[5] = make_double2(wd * q1, wd * q2);
-    if (A.self) {
+    if (A.self || A.alpha) {
       // e_r = n, e_theta = (ct cp, ct sp, -st), e_phi = (-sp, cp, 0)
       C[0 * nsn + kk] = aS * (f0 * n0 + f1 * n1 + f2 * n2);
       C[1 * nsn + kk] = aS * (f0 * ct * cp + f1 * ct * sp - f2 * st);
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
       C[5 * nsn + kk] = -q0 * sp + q1 * cp;
     }
   }
-  if (!A.self) {
+  if (!A.self && !A.alpha) {
     for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
     return;
   }
@@ -157,6 +159,16 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
     }
     double* o = ALPHA + 6 * it;
     o[0] = y0; o[1] = y1; o[2] = g0; o[3] = g1; o[4] = x0; o[5] = x1;
+    if (A.alpha) {
+      double2* g2 = reinterpret_cast<double2*>(A.alpha + (s * 2 * nlm + it) * 6);
+      g2[0] = make_double2(y0, y1);
+      g2[1] = make_double2(g0, g1);
+      g2[2] = make_double2(x0, x1);
+    }
+  }
+  if (!A.self) {
+    for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
+    return;
   }
   __syncthreads();
   // ---------------------------------------------------------------- C2

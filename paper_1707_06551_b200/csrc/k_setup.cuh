@@ -10,7 +10,7 @@ namespace bie {
 struct TableLayout {
   int p, nphi, nlm;  // nlm = (p+1)(p+2)/2 (n,m) pairs with m >= 0
   // offsets in doubles
-  int64_t t, st, wu, cph, sph, P, dP, mPs, lamS, lamD, total;
+  int64_t t, st, wu, cph, sph, P, dP, mPs, lamS, lamD, rA, rB, rC, total;
   __host__ __device__ explicit TableLayout(int p_) : p(p_) {
     nphi = 2 * p + 2;
     nlm = (p + 1) * (p + 2) / 2;
@@ -26,6 +26,9 @@ struct TableLayout {
     mPs = o;  o += int64_t(p + 1) * nlm;
     lamS = o; o += 3 * (p + 1);
     lamD = o; o += 3 * (p + 1);
+    rA = o;   o += nlm;  // normalised-Legendre recurrence coefficients per (n, m):
+    rB = o;   o += nlm;  //   P~_n = rA (t P~_{n-1} - rB P~_{n-2})
+    rC = o;   o += nlm;  //   sin(th) dP~_n/dth = n t P~_n - rC P~_{n-1}
     total = o;
   }
 };
@@ -119,6 +122,14 @@ __global__ void k_tables(int p, double* tab) {
     const double cnm = (n > m) ? sqrt((2.0 * n + 1.0) * ((double)n * n - (double)m * m) / (2.0 * n - 1.0)) : 0.0;
     const double prev = (n > m) ? pprev : 0.0;
     const int c = lm_index(p, n, m);
+    if (j == 0) {
+      tab[L.rA + c] = (n > m + 1) ? sqrt((4.0 * n * n - 1.0) / ((double)n * n - (double)m * m))
+                                  : (n == m + 1 ? sqrt(2.0 * m + 3.0) : 0.0);
+      tab[L.rB + c] = (n > m + 1) ? sqrt(((n - 1.0) * (n - 1.0) - (double)m * m) /
+                                         (4.0 * (n - 1.0) * (n - 1.0) - 1.0))
+                                  : 0.0;
+      tab[L.rC + c] = cnm;
+    }
     tab[L.P + (int64_t)j * L.nlm + c] = pcur;
     tab[L.dP + (int64_t)j * L.nlm + c] = (n * t * pcur - cnm * prev) / s;
     tab[L.mPs + (int64_t)j * L.nlm + c] = m * pcur / s;

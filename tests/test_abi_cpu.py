@@ -14,8 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def abi():
-    from paper_1707_06551_b200.build import build_lib
-    build_lib()
+    import __graft_entry__
+    __graft_entry__.build()
     from paper_1707_06551_b200 import _abi
     return _abi
 
