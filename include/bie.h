@@ -63,7 +63,8 @@ enum bie_status {
 #define BIE_KIND_OFFSURF 5  /* off-surface u,p pair sum (a7)                    */
 #define BIE_KIND_COPY 6     /* host<->device copies of the _host entry points   */
 #define BIE_KIND_NEAR 7     /* near-singular correction (NEXT-1)              */
-#define BIE_NUM_KINDS 8
+#define BIE_KIND_KRYLOV 8   /* GMRES vector kernels (NEXT-2)                  */
+#define BIE_NUM_KINDS 9
 
 /*
  * bie_create -- build nodes, weights, normals and spectral tables (row a1).
@@ -183,6 +184,29 @@ int bie_set_near(bie_ctx* ctx, double eta);
 
 /* Number of (target sphere, source sphere) near pairs of the current eta; -1 for NULL. */
 int64_t bie_near_pairs(const bie_ctx* ctx);
+
+/*
+ * bie_solve_porous -- Problem 1 of PAPER §5 (porous media, eqs 5.3-5.4,
+ * P:458-472): static spheres in an imposed flow u_inf; with the ansatz
+ * u = u_inf + sum_k (S_k + D_k)[mu] (eq 5.3) and no slip, solve the
+ * second-kind BIE (eq 5.4)
+ *     (1/2 I + sum_k (S_k + D_k)) [mu] = -u_inf     at every node
+ * by restarted GMRES(restart) with modified Gram-Schmidt (the paper names no
+ * solver; SPEC picks GMRES).  The operator is bie_apply_SLDL with f = q = mu
+ * (plus the near correction if bie_set_near is on) and the 1/2 I of the
+ * exterior limit (reading R14).  Dot products are fixed-order reductions, so
+ * the iterates are reproducible.
+ *   uinf [N][3] (device): imposed flow at the nodes; mu [N][3] (device) out.
+ *   Stops when the relative residual ||b - A mu|| / ||b|| <= tol or after
+ *   max_iter operator applications; *iters gets the count, *rel_resid the TRUE
+ *   relative residual of the returned mu (recomputed).  Not converging is
+ *   not an error (check *rel_resid).  Synchronous; workspace
+ *   (restart + 2) x 3N doubles is allocated per call.
+ *   The force on sphere s is -sum_{k in s} w_k mu_k (Stokes drag; pinned in
+ *   tests/test_oracle_porous.py).
+ */
+int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, int max_iter,
+                     int restart, int* iters, double* rel_resid, bie_stream_t s);
 
 /*
  * Tuning knob: number of source chunks of the far-field kernel (0 = automatic;

@@ -233,3 +233,27 @@ def near(centres, radii, p, mu, f, q, eta, subset=None):
 def apply_near(centres, radii, p, mu, f, q, eta, subset=None):
     """Composite apply with the near-singular correction: far + self + near."""
     return apply(centres, radii, p, mu, f, q, subset) + near(centres, radii, p, mu, f, q, eta, subset)
+
+
+# ---------------------------------------------------------------- NEXT-2
+def porous_matrix(centres, radii, p, mu, eta=0.0):
+    """Dense matrix of the second-kind operator of BIE 5.4,
+    A mu = (1/2) mu + sum_k (S_k + D_k)[mu] at every node, built column by
+    column from the oracle apply (+ near correction when eta > 0).  Small N only."""
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    A = np.empty((3 * N, 3 * N))
+    for col in range(3 * N):
+        e = np.zeros((N, 3))
+        e.reshape(-1)[col] = 1.0
+        col_u = apply(centres, radii, p, mu, e, e)
+        if eta > 0:
+            col_u = col_u + near(centres, radii, p, mu, e, e, eta)
+        A[:, col] = 0.5 * e.reshape(-1) + col_u.reshape(-1)
+    return A
+
+
+def solve_porous(centres, radii, p, mu, uinf, eta=0.0):
+    """Problem 1 (porous media, eqs 5.3-5.4): solve
+    (1/2 I + sum_k (S_k + D_k)) mu = -u_inf at the nodes by dense LU (numpy)."""
+    A = porous_matrix(centres, radii, p, mu, eta)
+    return np.linalg.solve(A, -np.asarray(uinf, dtype=np.float64).reshape(-1)).reshape(-1, 3)

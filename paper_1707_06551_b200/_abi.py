@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libbie.so")
 BIE_OK, BIE_ERR_ARG, BIE_ERR_GEOMETRY, BIE_ERR_ALLOC, BIE_ERR_CUDA, BIE_ERR_UNSUPPORTED = range(6)
 BIE_P_MAX = 30
 BIE_PART_FAR, BIE_PART_SELF = 1, 2
-KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near")
+KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov")
 BIE_NUM_KINDS = len(KINDS)
 
 #: every symbol include/bie.h declares (checked by tests/test_abi_cpu.py)
@@ -22,7 +22,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
-    "bie_set_near", "bie_near_pairs",
+    "bie_set_near", "bie_near_pairs", "bie_solve_porous",
     "bie_status_string", "bie_last_error",
 )
 
@@ -56,6 +56,8 @@ _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
 _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
 _lib.bie_near_pairs.restype = _i64
+_lib.bie_solve_porous.argtypes = [_vp, _vp, _vp, _d, _i32, _i32, ctypes.POINTER(_i32),
+                                  ctypes.POINTER(_d), _vp]
 _lib.bie_status_string.argtypes = [_i32]
 _lib.bie_status_string.restype = ctypes.c_char_p
 _lib.bie_last_error.argtypes = [_vp]
@@ -256,6 +258,17 @@ def bie_set_near(ctx, eta: float):
 
 def bie_near_pairs(ctx) -> int:
     return int(_lib.bie_near_pairs(ctx.handle))
+
+
+def bie_solve_porous(ctx, uinf, mu, tol=1e-12, max_iter=200, restart=50, stream=None):
+    """GMRES solve of BIE 5.4; returns (iterations, true relative residual)."""
+    N = bie_num_nodes(ctx)
+    it, res = ctypes.c_int(), ctypes.c_double()
+    _check(ctx, _lib.bie_solve_porous(ctx.handle, _ptr(uinf, device=True, n=3 * N),
+                                      _ptr(mu, device=True, n=3 * N), float(tol), int(max_iter),
+                                      int(restart), ctypes.byref(it), ctypes.byref(res),
+                                      _stream(stream)))
+    return it.value, res.value
 
 
 def bie_status_string(status: int) -> str:

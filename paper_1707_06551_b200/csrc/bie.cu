@@ -12,6 +12,7 @@
 
 #include "../../include/bie.h"
 #include "common.cuh"
+#include "k_krylov.cuh"
 #include "k_nbody.cuh"
 #include "k_near.cuh"
 #include "k_self.cuh"
@@ -734,6 +735,145 @@ int bie_set_near(bie_ctx* c, double eta) {
 }
 
 int64_t bie_near_pairs(const bie_ctx* c) { return c ? c->n_near_pairs : -1; }
+
+// ----------------------------------------------------------- NEXT-2 (GMRES)
+namespace {
+struct Krylov {
+  bie_ctx* c;
+  cudaStream_t s;
+  int64_t n;
+  double* part = nullptr;  // [kDotBlocks + 1]
+  double dot(const double* x, const double* y) {
+    Ev ev;
+    prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
+    k_dot_partial<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, y, part);
+    k_dot_final<<<1, kDotThreads, 0, s>>>(part, part + kDotBlocks);
+    prof_end(c, s, &ev);
+    double h = 0.0;
+    cudaMemcpyAsync(&h, part + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return h;
+  }
+  void axpby(double a, const double* x, double b, double* y) {
+    Ev ev;
+    prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
+    k_axpby<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, x, b, y);
+    prof_end(c, s, &ev);
+  }
+  // y = (1/2 I + S + D_pv (+ near correction)) x     (BIE 5.4)
+  int op(const double* x, double* y) {
+    int rc = run_apply(c, x, x, y, BIE_PART_FAR | BIE_PART_SELF, s);
+    if (rc) return rc;
+    axpby(0.5, x, 1.0, y);
+    return launch_check(c, "k_axpby");
+  }
+};
+}  // namespace
+
+int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol, int max_iter,
+                     int restart, int* iters_out, double* resid_out, bie_stream_t st) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (!uinf || !mu_out || !is_device_ptr(uinf) || !is_device_ptr(mu_out))
+    return fail(c, BIE_ERR_ARG, "uinf and mu must be device pointers%s");
+  const int64_t n = 3 * c->N;
+  if (overlaps(uinf, n, mu_out, n)) return fail(c, BIE_ERR_ARG, "mu overlaps uinf%s");
+  if (!(tol > 0.0) || max_iter < 1 || restart < 1 || restart > 500)
+    return fail(c, BIE_ERR_ARG, "need tol > 0, max_iter >= 1, 1 <= restart <= 500%s");
+  Krylov K{c, (cudaStream_t)st, n};
+  const int m = restart;
+  double *V = nullptr, *w = nullptr, *b = nullptr;
+  if (cudaMalloc(&V, (size_t)(m + 1) * n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&w, n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&b, n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&K.part, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(K.part);
+    return fail(c, BIE_ERR_ALLOC, "GMRES workspace%s");
+  }
+  auto cleanup = [&]() { cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(K.part); };
+  // b = -u_inf, x0 = 0
+  cudaMemsetAsync(mu_out, 0, n * sizeof(double), K.s);
+  cudaMemsetAsync(b, 0, n * sizeof(double), K.s);
+  K.axpby(-1.0, uinf, 0.0, b);
+  const double bnorm = std::sqrt(K.dot(b, b));
+  int it = 0;
+  double rel = 0.0;
+  if (bnorm == 0.0) {
+    cleanup();
+    if (iters_out) *iters_out = 0;
+    if (resid_out) *resid_out = 0.0;
+    return BIE_OK;
+  }
+  std::vector<double> H((size_t)(m + 1) * m), g(m + 1), cs(m), sn(m), y(m);
+  bool done = false;
+  while (!done) {
+    // r = b - A x  -> V[0]
+    double* v0 = V;
+    if ((rc = K.op(mu_out, w))) { cleanup(); return rc; }
+    cudaMemcpyAsync(v0, b, n * sizeof(double), cudaMemcpyDeviceToDevice, K.s);
+    K.axpby(-1.0, w, 1.0, v0);
+    const double beta = std::sqrt(K.dot(v0, v0));
+    rel = beta / bnorm;
+    if (rel <= tol || it >= max_iter) break;
+    K.axpby(0.0, v0, 1.0 / beta, v0);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    for (; j < m && it < max_iter; ++j, ++it) {
+      double* vj = V + (size_t)j * n;
+      double* vn = V + (size_t)(j + 1) * n;
+      if ((rc = K.op(vj, vn))) { cleanup(); return rc; }
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        const double h = K.dot(vn, V + (size_t)i * n);
+        H[(size_t)i * m + j] = h;
+        K.axpby(-h, V + (size_t)i * n, 1.0, vn);
+      }
+      const double hn = std::sqrt(K.dot(vn, vn));
+      H[(size_t)(j + 1) * m + j] = hn;
+      if (hn > 0.0) K.axpby(0.0, vn, 1.0 / hn, vn);
+      for (int i = 0; i < j; ++i) {  // apply previous Givens rotations
+        const double a1 = H[(size_t)i * m + j], a2 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a1 + sn[i] * a2;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a1 + cs[i] * a2;
+      }
+      const double a1 = H[(size_t)j * m + j], a2 = H[(size_t)(j + 1) * m + j];
+      const double den = std::hypot(a1, a2);
+      cs[j] = den > 0.0 ? a1 / den : 1.0;
+      sn[j] = den > 0.0 ? a2 / den : 0.0;
+      H[(size_t)j * m + j] = den;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rel = std::fabs(g[j + 1]) / bnorm;
+      if (rel <= tol || hn == 0.0) {
+        ++j;
+        ++it;
+        done = true;
+        break;
+      }
+    }
+    // x += V y,  H[0:j,0:j] y = g[0:j]
+    for (int i = j - 1; i >= 0; --i) {
+      double sacc = g[i];
+      for (int k = i + 1; k < j; ++k) sacc -= H[(size_t)i * m + k] * y[k];
+      y[i] = sacc / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < j; ++i) K.axpby(y[i], V + (size_t)i * n, 1.0, mu_out);
+    if (it >= max_iter) done = true;
+  }
+  // true relative residual of the returned iterate
+  if ((rc = K.op(mu_out, w))) { cleanup(); return rc; }
+  K.axpby(1.0, b, -1.0, w);
+  rel = std::sqrt(K.dot(w, w)) / bnorm;
+  cleanup();
+  if (iters_out) *iters_out = it;
+  if (resid_out) *resid_out = rel;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, "bie_solve_porous");
+  return BIE_OK;
+}
 
 int bie_set_source_chunks(bie_ctx* c, int chunks) {
   if (!c) return BIE_ERR_ARG;

@@ -1,0 +1,54 @@
+// k_krylov.cuh -- vector kernels of the GMRES solve of BIE 5.4 (NEXT-2).
+// Dot products use a fixed grid and a fixed-order two-pass reduction, so
+// every Krylov iterate is bitwise reproducible run to run.
+#pragma once
+#include "common.cuh"
+
+namespace bie {
+
+constexpr int kDotBlocks = 592;  // 4 x 148 SMs; fixed => deterministic
+constexpr int kDotThreads = 256;
+
+// y = a x + b y
+__global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b,
+                        double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], b * y[i]);
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// part[b] = sum over the grid-stride slice of block b of x_i y_i
+__global__ void __launch_bounds__(kDotThreads) k_dot_partial(int64_t n, const double* __restrict__ x,
+                                                             const double* __restrict__ y,
+                                                             double* __restrict__ part) {
+  __shared__ double red[kDotThreads / 32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kDotThreads + threadIdx.x; i < n;
+       i += (int64_t)kDotBlocks * kDotThreads)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// out[0] = sum_b part[b] in fixed order
+__global__ void __launch_bounds__(kDotThreads) k_dot_final(const double* __restrict__ part,
+                                                           double* __restrict__ out) {
+  __shared__ double red[kDotThreads / 32];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < kDotBlocks; b += kDotThreads) s += part[b];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+}  // namespace bie
