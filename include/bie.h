@@ -64,7 +64,8 @@ enum bie_status {
 #define BIE_KIND_COPY 6     /* host<->device copies of the _host entry points   */
 #define BIE_KIND_NEAR 7     /* near-singular correction (NEXT-1)              */
 #define BIE_KIND_KRYLOV 8   /* GMRES vector kernels (NEXT-2)                  */
-#define BIE_NUM_KINDS 9
+#define BIE_KIND_KFAR 9     /* far-field traction operator K pair sum (NEXT-3) */
+#define BIE_NUM_KINDS 10
 
 /*
  * bie_create -- build nodes, weights, normals and spectral tables (row a1).
@@ -129,6 +130,19 @@ int bie_apply_DL(bie_ctx* ctx, const double* q, double* u, bie_stream_t s);
  */
 int bie_apply_parts(bie_ctx* ctx, const double* f, const double* q, double* u, int parts,
                     bie_stream_t s);
+
+/*
+ * bie_apply_K -- u = K_pv[sigma] at every node: the traction
+ * of the single layer (eq 2.22) with the target normal,
+ *     K[s](x) = -(3/(4 pi)) int ((x-y).n(x)) ((x-y).s(y)) (x-y)/|x-y|^5 dS_y
+ * (reading R21: the adjoint of the R1 double layer, as P:219 requires),
+ * smooth rule over every other sphere + the principal-value self term, whose
+ * spectrum is that of D_pv (K_+ = D_-, K_- = D_+).  The one-sided
+ * tractions are K_pv -+ sigma/2 (exterior: minus).  `parts` as in
+ * bie_apply_parts.  The near correction (bie_set_near) does not apply to K.
+ * sigma, u: device [N][3]; u must not overlap sigma.
+ */
+int bie_apply_K(bie_ctx* ctx, const double* sigma, double* u, int parts, bie_stream_t s);
 
 /*
  * bie_eval_offsurface -- velocity and pressure at m arbitrary targets (row a7).

@@ -257,3 +257,48 @@ def solve_porous(centres, radii, p, mu, uinf, eta=0.0):
     (1/2 I + sum_k (S_k + D_k)) mu = -u_inf at the nodes by dense LU (numpy)."""
     A = porous_matrix(centres, radii, p, mu, eta)
     return np.linalg.solve(A, -np.asarray(uinf, dtype=np.float64).reshape(-1)).reshape(-1, 3)
+
+
+# ---------------------------------------------------------------- NEXT-3
+def _load_K():
+    lib = _load()
+    if not getattr(lib, "_K_ready", False):
+        i64, i32 = ctypes.c_int64, ctypes.c_int
+        lib.oracle_far_K.argtypes = [_DP, _DP, i64, i32, _DP, _I64P, i64, _DP]
+        lib.oracle_K_at.argtypes = [_DP, _DP, i64, i32, _DP, _DP, _DP, i64, _DP]
+        lib._K_ready = True
+    return lib
+
+
+def far_K(centres, radii, p, sigma, subset=None):
+    """Smooth-rule traction operator K (eq 2.22, reading R21) over all other
+    spheres, at nodes `subset` (target normal = the node's outward normal)."""
+    lib = _load_K()
+    centres, radii, sigma = _c(centres), _c(radii), _c(sigma)
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    idx = _subset(subset, N)
+    u = np.empty((len(idx), 3))
+    if lib.oracle_far_K(_dp(centres), _dp(radii), len(radii), p, _dp(sigma),
+                        idx.ctypes.data_as(_I64P), len(idx), _dp(u)):
+        raise ValueError("far_K: bad arguments")
+    return u
+
+
+def K_at(centres, radii, p, sigma, targets, normals):
+    """Smooth-rule K[sigma] at arbitrary points with given unit normals (all sources)."""
+    lib = _load_K()
+    centres, radii, sigma, targets, normals = (_c(centres), _c(radii), _c(sigma), _c(targets),
+                                               _c(normals))
+    u = np.empty((targets.shape[0], 3))
+    if lib.oracle_K_at(_dp(centres), _dp(radii), len(radii), p, _dp(sigma), _dp(targets),
+                       _dp(normals), targets.shape[0], _dp(u)):
+        raise ValueError("K_at: bad arguments")
+    return u
+
+
+def apply_K(centres, radii, p, sigma, subset=None):
+    """Discrete K_pv[sigma] at nodes: smooth far field + self term with the
+    principal-value spectrum of K, which P:219 fixes as that of D_pv
+    (K_+ = D_-, K_- = D_+  =>  K_pv = D_pv)."""
+    return (far_K(centres, radii, p, sigma, subset) +
+            self_term(centres, radii, p, 1.0, None, sigma, subset))

@@ -669,3 +669,70 @@ extern "C" int oracle_near(const double* centres, const double* radii, int64_t n
   }
   return 0;
 }
+
+// ============================================================ NEXT-3 (K)
+// Traction of the single layer (eq 2.22):
+//   K[s](x)_i = int T_ijk(x,y) n_k(x) s_j(y) dS_y,
+// with the TARGET normal n(x).  The sign of T in eq 2.20 is ambiguous (reading
+// R1 fixed it for D with the source normal); for K the reading is
+//   K[s](x) = -(3/(4 pi)) int ((x-y).n(x)) ((x-y).s(y)) (x-y) / |x-y|^5 dS_y,
+// i.e. the L2 adjoint of D, which is what P:219 ("the spectra of K+ matches
+// that of D- and K- that of D+") requires: K_pv = D_pv on the sphere
+// (reading R21, pinned by brute-force quadrature and the translating-sphere
+// traction in tests/test_oracle_traction.py).
+//
+// Far field of K at the subset nodes tidx (own sphere excluded, Neumaier).
+extern "C" int oracle_far_K(const double* centres, const double* radii, int64_t ns, int p,
+                            const double* sigma, const int64_t* tidx, int64_t nt, double* u) {
+  if (ns < 1 || p < 1 || !sigma || !u || !tidx) return 1;
+  Geometry G(centres, radii, ns, p);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t i = tidx[t];
+    const int64_t si = i / G.nsn;
+    const double* x = &G.x[3 * i];
+    const double* nx = &G.n[3 * i];
+    Neumaier acc[3];
+    for (int64_t k = 0; k < G.N; ++k) {
+      if (k / G.nsn == si) continue;
+      const double* y = &G.x[3 * k];
+      const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
+      const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
+      const double r = std::sqrt(r2);
+      const double r5 = r2 * r2 * r;
+      const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
+      const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
+      const double cK = -3.0 * G.w[k] / (4.0 * PI);
+      for (int c = 0; c < 3; ++c) acc[c].add(cK * rn * rs * rho[c] / r5);
+    }
+    for (int c = 0; c < 3; ++c) u[3 * t + c] = acc[c].get();
+  }
+  return 0;
+}
+
+// Off-surface version with an explicit target normal (used by the pins).
+extern "C" int oracle_K_at(const double* centres, const double* radii, int64_t ns, int p,
+                           const double* sigma, const double* targets, const double* normals,
+                           int64_t m, double* u) {
+  if (ns < 1 || p < 1 || !sigma || (m > 0 && (!targets || !normals || !u))) return 1;
+  Geometry G(centres, radii, ns, p);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < m; ++t) {
+    const double* x = targets + 3 * t;
+    const double* nx = normals + 3 * t;
+    Neumaier acc[3];
+    for (int64_t k = 0; k < G.N; ++k) {
+      const double* y = &G.x[3 * k];
+      const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
+      const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
+      const double r = std::sqrt(r2);
+      const double r5 = r2 * r2 * r;
+      const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
+      const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
+      const double cK = -3.0 * G.w[k] / (4.0 * PI);
+      for (int c = 0; c < 3; ++c) acc[c].add(cK * rn * rs * rho[c] / r5);
+    }
+    for (int c = 0; c < 3; ++c) u[3 * t + c] = acc[c].get();
+  }
+  return 0;
+}

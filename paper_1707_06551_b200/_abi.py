@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libbie.so")
 BIE_OK, BIE_ERR_ARG, BIE_ERR_GEOMETRY, BIE_ERR_ALLOC, BIE_ERR_CUDA, BIE_ERR_UNSUPPORTED = range(6)
 BIE_P_MAX = 30
 BIE_PART_FAR, BIE_PART_SELF = 1, 2
-KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov")
+KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov", "kfar")
 BIE_NUM_KINDS = len(KINDS)
 
 #: every symbol include/bie.h declares (checked by tests/test_abi_cpu.py)
@@ -22,7 +22,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
-    "bie_set_near", "bie_near_pairs", "bie_solve_porous",
+    "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K",
     "bie_status_string", "bie_last_error",
 )
 
@@ -56,6 +56,7 @@ _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
 _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
 _lib.bie_near_pairs.restype = _i64
+_lib.bie_apply_K.argtypes = [_vp, _vp, _vp, _i32, _vp]
 _lib.bie_solve_porous.argtypes = [_vp, _vp, _vp, _d, _i32, _i32, ctypes.POINTER(_i32),
                                   ctypes.POINTER(_d), _vp]
 _lib.bie_status_string.argtypes = [_i32]
@@ -202,6 +203,13 @@ def bie_apply_parts(ctx, f, q, u, parts: int, stream=None):
     _check(ctx, _lib.bie_apply_parts(ctx.handle, _ptr(f, device=True, n=3 * N),
                                      _ptr(q, device=True, n=3 * N), _ptr(u, device=True, n=3 * N),
                                      int(parts), _stream(stream)))
+
+
+def bie_apply_K(ctx, sigma, u, parts=BIE_PART_FAR | BIE_PART_SELF, stream=None):
+    """u = K_pv[sigma] (traction operator, NEXT-3)."""
+    N = bie_num_nodes(ctx)
+    _check(ctx, _lib.bie_apply_K(ctx.handle, _ptr(sigma, device=True, n=3 * N),
+                                 _ptr(u, device=True, n=3 * N), int(parts), _stream(stream)))
 
 
 def bie_eval_offsurface(ctx, f, q, targets, u, p=None, stream=None):

@@ -33,6 +33,7 @@ constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 
 #define NBODY_APPLY k_nbody<kR, kTPB, kTS, kNST, false, 1, 2>
 #define NBODY_OFF k_nbody<kR, kTPB, kTS, kNST, true, 1, 1>
+#define NBODY_K k_nbody<kR, kTPB, kTS, kNST, false, 1, 2, 1>
 
 struct Ev {
   int kind;
@@ -42,7 +43,7 @@ struct Ev {
 }  // namespace
 
 struct bie_ctx {
-  int dev = -1, sm_count = 0, occ_apply = 1, occ_off = 1;
+  int dev = -1, sm_count = 0, occ_apply = 1, occ_off = 1, occ_K = 1;
   int p = 0, nsn = 0;
   int64_t ns = 0, N = 0;
   double mu = 1.0;
@@ -245,7 +246,7 @@ static int launch_check(bie_ctx* c, const char* what) {
   return BIE_OK;
 }
 
-static int run_far(bie_ctx* c, double* u, cudaStream_t s);
+static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode = 0);
 
 static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
                      cudaStream_t s) {
@@ -295,10 +296,11 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
 }
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
-static int run_far(bie_ctx* c, double* u, cudaStream_t s) {
+static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode) {
   Ev ev;
   int rc;
-  const ChunkPlan P = plan_chunks(c, c->N, c->N, c->occ_apply);
+  const ChunkPlan P = plan_chunks(c, c->N, c->N, mode ? c->occ_K : c->occ_apply);
+  const int kind = mode ? BIE_KIND_KFAR : BIE_KIND_NBODY;
   NbodyArgs A;
   A.rec = c->d_rec;
   A.qn3 = nullptr;
@@ -315,8 +317,9 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s) {
   if (P.n_chunks == 1) {
     A.uinit = u;
     A.uout = u;
-    prof_begin(c, BIE_KIND_NBODY, s, &ev);
-    NBODY_APPLY<<<(unsigned)P.n_tt, kTPB, nb_smem, s>>>(A);
+    prof_begin(c, kind, s, &ev);
+    if (mode) NBODY_K<<<(unsigned)P.n_tt, kTPB, nb_smem, s>>>(A);
+    else NBODY_APPLY<<<(unsigned)P.n_tt, kTPB, nb_smem, s>>>(A);
     prof_end(c, s, &ev);
     return launch_check(c, "k_nbody");
   }
@@ -324,8 +327,9 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s) {
   if (rc) return rc;
   A.uinit = nullptr;
   A.uout = c->d_part;
-  prof_begin(c, BIE_KIND_NBODY, s, &ev);
-  NBODY_APPLY<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
+  prof_begin(c, kind, s, &ev);
+  if (mode) NBODY_K<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
+  else NBODY_APPLY<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
   prof_end(c, s, &ev);
   rc = launch_check(c, "k_nbody");
   if (rc) return rc;
@@ -490,6 +494,8 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
                                                 NbodySmem<kTS, kNST, true>::kBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_K, NBODY_K, kTPB,
+                                                NbodySmem<kTS, kNST, false>::kBytes);
   e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -537,6 +543,40 @@ int bie_apply_parts(bie_ctx* c, const double* f, const double* q, double* u, int
   if (overlaps(u, n3, f, n3) || overlaps(u, n3, q, n3))
     return fail(c, BIE_ERR_ARG, "output u overlaps an input%s");
   return run_apply(c, f, q, u, parts, (cudaStream_t)s);
+}
+
+int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_stream_t st) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (parts <= 0 || parts > (BIE_PART_FAR | BIE_PART_SELF))
+    return fail(c, BIE_ERR_ARG, "parts must be a non-empty subset of FAR|SELF%s");
+  const int64_t n3 = 3 * c->N;
+  if (!sigma || !u || !is_device_ptr(sigma) || !is_device_ptr(u))
+    return fail(c, BIE_ERR_ARG, "sigma and u must be device pointers%s");
+  if (overlaps(u, n3, sigma, n3)) return fail(c, BIE_ERR_ARG, "output u overlaps sigma%s");
+  cudaStream_t s = (cudaStream_t)st;
+  // self term: K_pv has the D_pv spectrum; packs q' = (3/4pi) w sigma
+  SelfArgs SA;
+  SA.p = c->p;
+  SA.ns = c->ns;
+  SA.mu = c->mu;
+  SA.tab = c->d_tab;
+  SA.centres = c->d_centres;
+  SA.radii = c->d_radii;
+  SA.f = nullptr;
+  SA.q = sigma;
+  SA.u = u;
+  SA.rec = c->d_rec;
+  SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
+  SA.alpha = nullptr;
+  Ev ev;
+  prof_begin(c, BIE_KIND_SELF, s, &ev);
+  k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
+  prof_end(c, s, &ev);
+  rc = launch_check(c, "k_self");
+  if (rc || !(parts & BIE_PART_FAR)) return rc;
+  return run_far(c, u, s, 1);
 }
 
 int bie_apply_SLDL(bie_ctx* c, const double* f, const double* q, double* u, bie_stream_t s) {

@@ -72,7 +72,32 @@ __device__ __forceinline__ void pair_acc(const double2 s0, const double2 s1, con
   if (OFF) pacc = fma(fma(-qn, y2, sp), y, pacc);
 }
 
-template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2>
+// Traction operator K (NEXT-3, eq 2.22 with reading R21): target normal nx,
+//   u_i -= (rho.n_x)(rho.q'_k) rho y^5,  q' = (3/(4 pi)) w sigma  (25 FP64 ops).
+template <bool MASK>
+__device__ __forceinline__ void pair_K(const double2 s0, const double2 s1, const double2 s4,
+                                       const double2 s5, const double* xt, const double* nx,
+                                       double* acc, int k, int lo, int nsn) {
+  const double dx = xt[0] - s0.x, dy = xt[1] - s0.y, dz = xt[2] - s1.x;
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  double y = y0 * fma(e, fma(e, 0.375, 0.5), 1.0);
+  if (MASK) {
+    if ((unsigned)(k - lo) < (unsigned)nsn) y = 0.0;  // own sphere: excluded (R8)
+  }
+  const double rq = fma(dz, s5.y, fma(dy, s5.x, dx * s4.y));
+  const double rn = fma(dz, nx[2], fma(dy, nx[1], dx * nx[0]));
+  const double y2 = y * y;
+  const double t = (rn * rq) * (y2 * y2);
+  const double sm = -t * y;
+  acc[0] = fma(dx, sm, acc[0]);
+  acc[1] = fma(dy, sm, acc[1]);
+  acc[2] = fma(dz, sm, acc[2]);
+}
+
+// MODE 0: S + D (rows a3, a7); MODE 1: traction operator K (apply only).
+template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0>
 __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   using SM = NbodySmem<TS, NST, OFF>;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -87,6 +112,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
 
   // ---- targets held in registers
   double xt[R][3], acc[R][3], pacc[R];
+  double nx[MODE == 1 ? R : 1][3];
   int lo[R];
   int64_t tidx[R];
 #pragma unroll
@@ -104,6 +130,11 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
       xt[r][1] = A.rec[ic * kRec + 1];
       xt[r][2] = A.rec[ic * kRec + 2];
       lo[r] = (int)((ic / A.nsn) * A.nsn);
+      if (MODE == 1) {
+        nx[MODE == 1 ? r : 0][0] = A.rec[ic * kRec + 3];
+        nx[MODE == 1 ? r : 0][1] = A.rec[ic * kRec + 4];
+        nx[MODE == 1 ? r : 0][2] = A.rec[ic * kRec + 5];
+      }
     }
     acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
     pacc[r] = 0.0;
@@ -150,8 +181,12 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
         const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
         const double qn = OFF ? sqn[sidx] : 0.0;
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          pair_acc<false, OFF>(s0, s1, s2, s3, s4, s5, qn, xt[r], acc[r], pacc[r], 0, 0, 1);
+        for (int r = 0; r < R; ++r) {
+          if (MODE == 1)
+            pair_K<false>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], 0, 0, 1);
+          else
+            pair_acc<false, OFF>(s0, s1, s2, s3, s4, s5, qn, xt[r], acc[r], pacc[r], 0, 0, 1);
+        }
       }
     } else {
       for (int sidx = 0; sidx < cnt; ++sidx) {
@@ -159,9 +194,13 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
         const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
         const int k = (int)(k0 + sidx);
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], k, lo[r],
-                                A.nsn);
+        for (int r = 0; r < R; ++r) {
+          if (MODE == 1)
+            pair_K<true>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], k, lo[r], A.nsn);
+          else
+            pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], k, lo[r],
+                                  A.nsn);
+        }
       }
     }
     __syncthreads();  // every thread is done with stage st

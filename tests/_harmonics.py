@@ -82,6 +82,11 @@ def onsurface_layers(xt, centre, a, mu, dens, kind, nalpha=72, nbeta=144):
     if kind == "S":
         rf = np.einsum("...c,...c->...", rho, g)
         K = (g / r[..., None] + rf[..., None] * rho / r[..., None] ** 3) / (8.0 * np.pi * mu)
+    elif kind == "K":
+        # traction of the single layer with the TARGET normal xh (eq 2.22, reading R21)
+        rn = rho @ xh
+        rq = np.einsum("...c,...c->...", rho, g)
+        K = -3.0 / (4.0 * np.pi) * (rn * rq)[..., None] * rho / r[..., None] ** 5
     else:
         rn = np.einsum("...c,...c->...", rho, yh)
         rq = np.einsum("...c,...c->...", rho, g)
