@@ -302,3 +302,44 @@ def apply_K(centres, radii, p, sigma, subset=None):
     (K_+ = D_-, K_- = D_+  =>  K_pv = D_pv)."""
     return (far_K(centres, radii, p, sigma, subset) +
             self_term(centres, radii, p, 1.0, None, sigma, subset))
+
+
+def _load_near_off():
+    lib = _load_near()
+    if not getattr(lib, "_near_off_ready", False):
+        i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        lib.oracle_exterior_pressure.argtypes = [i32, _DP, d, d, _DP, _DP, _DP, i64, _DP]
+        lib.oracle_near_offsurface.argtypes = [_DP, _DP, i64, i32, d, _DP, _DP, d, _DP, i64, _DP, _DP]
+        lib._near_off_ready = True
+    return lib
+
+
+def exterior_pressure(p, centre, a, mu, f_s, q_s, targets):
+    """Exterior pressure of ONE sphere's expansion (D per reading R12)."""
+    lib = _load_near_off()
+    c = _c(np.asarray(centre, dtype=np.float64).reshape(3))
+    f_s, q_s, targets = _c(f_s), _c(q_s), _c(targets)
+    pr = np.empty(targets.shape[0])
+    if lib.oracle_exterior_pressure(p, _dp(c), a, mu, _dp(f_s), _dp(q_s), _dp(targets),
+                                    targets.shape[0], _dp(pr)):
+        raise ValueError("exterior_pressure: bad arguments")
+    return pr
+
+
+def near_offsurface(centres, radii, p, mu, f, q, eta, targets):
+    """Near correction (du, dp) at arbitrary targets (point-to-surface eq 4.5)."""
+    lib = _load_near_off()
+    centres, radii, f, q, targets = _c(centres), _c(radii), _c(f), _c(q), _c(targets)
+    M = targets.shape[0]
+    du, dp = np.empty((M, 3)), np.empty(M)
+    if lib.oracle_near_offsurface(_dp(centres), _dp(radii), len(radii), p, mu, _dp(f), _dp(q), eta,
+                                  _dp(targets), M, _dp(du), _dp(dp)):
+        raise ValueError("near_offsurface: bad arguments")
+    return du, dp
+
+
+def offsurface_near(centres, radii, p, mu, f, q, eta, targets):
+    """Corrected off-surface evaluator: smooth sum + near correction."""
+    u, pr = offsurface(centres, radii, p, mu, f, q, targets)
+    du, dp = near_offsurface(centres, radii, p, mu, f, q, eta, targets)
+    return u + du, pr + dp

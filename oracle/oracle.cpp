@@ -736,3 +736,110 @@ extern "C" int oracle_K_at(const double* centres, const double* radii, int64_t n
   }
   return 0;
 }
+
+// ============================================ NEXT-1 for off-surface targets
+// Exterior pressure of a sphere's expansion: only the W_n channels carry
+// pressure outside (P:189 for S: n Y_n r^{-n-1}; the D value 2n(n-1) Y_n
+// r^{-n-1} replaces the inconsistent P:215 per reading R12).  Scalings
+// (R5, R6): S pressure is a- and mu-free for the unscaled density, D pressure
+// carries mu/a.  With alpha_f = projections of (a/mu) f:
+//   p = sum_{n,m} (mu/a) [ n alpha_W[(a/mu) f] + 2n(n-1) alpha_W[q] ] Y_n^m r^{-n-1}.
+static double exterior_pressure(int p, const double* c, double a, double mu,
+                                const std::vector<cplx>* af, const std::vector<cplx>* aq,
+                                const double* x) {
+  const double rv[3] = {(x[0] - c[0]) / a, (x[1] - c[1]) / a, (x[2] - c[2]) / a};
+  const double r = std::sqrt(rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2]);
+  const double th = std::acos(rv[2] / r), ph = std::atan2(rv[1], rv[0]);
+  cplx acc = 0.0;
+  for (int n = 1; n <= p; ++n)
+    for (int m = -n; m <= n; ++m) {
+      cplx Y, dY, dYp;
+      ynm_all(n, m, th, ph, &Y, &dY, &dYp);
+      const size_t ix = (size_t)(n * n + n + m) * 3 + 1;  // W channel
+      cplx coef = 0.0;
+      if (af) coef += (double)n * (*af)[ix];
+      if (aq) coef += 2.0 * n * (n - 1.0) * (*aq)[ix];
+      acc += (mu / a) * coef * Y * std::pow(r, -n - 1.0);
+    }
+  return acc.real();
+}
+
+extern "C" int oracle_exterior_pressure(int p, const double* c, double a, double mu,
+                                        const double* f_s, const double* q_s,
+                                        const double* targets, int64_t m, double* pr) {
+  if (p < 1 || !(a > 0) || !(mu > 0) || !c || (m > 0 && (!targets || !pr))) return 1;
+  std::vector<cplx> af, aq;
+  if (f_s) {  // projections of (a/mu) f, as in the velocity path
+    std::vector<double> g(3 * (p + 1) * (2 * p + 2));
+    for (size_t k = 0; k < g.size(); ++k) g[k] = (a / mu) * f_s[k];
+    project_sphere(p, g.data(), af);
+  }
+  if (q_s) project_sphere(p, q_s, aq);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < m; ++t)
+    pr[t] = exterior_pressure(p, c, a, mu, f_s ? &af : nullptr, q_s ? &aq : nullptr, targets + 3 * t);
+  return 0;
+}
+
+// Near correction at arbitrary targets: target x and sphere s are near when
+// the point-to-surface distance |x - c_s| - a_s < eta * 2 a_s (eq 4.5 with
+// the target as a point: SPEC's "point-to-surface distance for target
+// batches").  du, dp = sum over near s of [exterior - smooth] (velocity and
+// pressure).  The corrected evaluator is oracle_offsurface + this.
+extern "C" int oracle_near_offsurface(const double* centres, const double* radii, int64_t ns, int p,
+                                      double mu, const double* f, const double* q, double eta,
+                                      const double* targets, int64_t m, double* du, double* dp) {
+  if (ns < 1 || p < 1 || !(mu > 0) || !(eta >= 0) || (m > 0 && (!targets || !du))) return 1;
+  Geometry G(centres, radii, ns, p);
+  const int nsn = G.nsn;
+  auto near_pt = [&](int64_t s, const double* x) {
+    const double dx = x[0] - centres[3 * s], dy = x[1] - centres[3 * s + 1], dz = x[2] - centres[3 * s + 2];
+    return std::sqrt(dx * dx + dy * dy + dz * dz) - radii[s] < eta * 2.0 * radii[s];
+  };
+  std::vector<char> need(ns, 0);
+  for (int64_t t = 0; t < m; ++t)
+    for (int64_t s = 0; s < ns; ++s)
+      if (near_pt(s, targets + 3 * t)) need[s] = 1;
+  std::vector<std::vector<cplx>> AF(ns), AQ(ns);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = 0; s < ns; ++s) {
+    if (!need[s]) continue;
+    if (f) {
+      std::vector<double> g(3 * nsn);
+      for (int k = 0; k < 3 * nsn; ++k) g[k] = (radii[s] / mu) * f[3 * s * nsn + k];
+      project_sphere(p, g.data(), AF[s]);
+    }
+    if (q) project_sphere(p, q + 3 * s * nsn, AQ[s]);
+  }
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < m; ++t) {
+    const double* x = targets + 3 * t;
+    double acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
+    for (int64_t s = 0; s < ns; ++s) {
+      if (!near_pt(s, x)) continue;
+      double ue[3];
+      // exterior_eval scales alpha_f by a/mu itself; pass unscaled projections
+      std::vector<cplx> afu;
+      if (f) {
+        afu = AF[s];
+        for (auto& v : afu) v *= mu / radii[s];
+      }
+      exterior_eval(p, centres + 3 * s, radii[s], mu, f ? &afu : nullptr, q ? &AQ[s] : nullptr, x, ue);
+      const double pe = exterior_pressure(p, centres + 3 * s, radii[s], mu, f ? &AF[s] : nullptr,
+                                          q ? &AQ[s] : nullptr, x);
+      Neumaier sm[3], sp;
+      for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
+        double v[3], pv;
+        pair_terms(x, &G.x[3 * k], &G.n[3 * k], G.w[k], f ? f + 3 * k : nullptr,
+                   q ? q + 3 * k : nullptr, mu, v, &pv);
+        for (int c = 0; c < 3; ++c) sm[c].add(v[c]);
+        sp.add(pv);
+      }
+      for (int c = 0; c < 3; ++c) acc[c] += ue[c] - sm[c].get();
+      pacc += pe - sp.get();
+    }
+    for (int c = 0; c < 3; ++c) du[3 * t + c] = acc[c];
+    if (dp) dp[t] = pacc;
+  }
+  return 0;
+}

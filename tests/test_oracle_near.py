@@ -131,3 +131,67 @@ def test_near_corrected_apply_rigid_modes(oracle_mod):
     Ue = (d @ U)[:, None]
     ref = 0.75 * (U / rr + Ue * d / rr) + 0.25 * (U / rr ** 3 - 3 * Ue * d / rr ** 3)
     assert np.abs(u - ref).max() <= 1e-13
+
+
+# ------------------------------------------------- off-surface targets (a7)
+def test_exterior_pressure_translating_sphere(oracle_mod):
+    """p = 3 mu a U.(x-c)/(2 r^3) outside a translating sphere (classical; P:189
+    S[W_1] case) down to r = 1.01 a."""
+    p, a, mu = 8, 1.3, 1.7
+    c = np.array([0.2, -0.1, 0.4])
+    U = np.array([0.3, -1.0, 0.5])
+    x, _, _ = oracle_mod.nodes(c[None], np.array([a]), p)
+    f = np.tile(3 * mu * U / (2 * a), (len(x), 1))
+    d = _dirs(6, 12)
+    rr = np.random.default_rng(7).uniform(1.01, 1.3, 12) * a
+    pr = oracle_mod.exterior_pressure(p, c, a, mu, f, None, c + d * rr[:, None])
+    assert np.abs(pr - 1.5 * mu * a * (d @ U) / rr ** 2).max() <= 1e-13
+
+
+@pytest.mark.parametrize("gap", [0.5, 0.3])
+def test_exterior_pressure_matches_bruteforce(oracle_mod, gap):
+    """Band-limited S and D densities: spectral exterior pressure == converged
+    (p_src = 96) smooth-rule pressure (whose kernels are pinned by the Stokes
+    equations in test_oracle_pins.py)."""
+    p, a, mu = 8, 1.3, 1.7
+    c = np.array([0.2, -0.1, 0.4])
+
+    def dens(y):
+        return sum(H.vsh_density(n, m, ch, y, c, a)
+                   for n, m, ch in [(1, 0, 1), (2, 1, 1), (3, -2, 1), (4, 3, 0), (2, 0, 2), (5, 2, 1)])
+
+    x, _, _ = oracle_mod.nodes(c[None], np.array([a]), p)
+    tg = c + _dirs(8, 10) * (a + gap)
+    pe = oracle_mod.exterior_pressure(p, c, a, mu, dens(x), dens(x), tg)
+    xs, _, _ = oracle_mod.nodes(c[None], np.array([a]), 96)
+    _, pb = oracle_mod.offsurface(c[None], np.array([a]), 96, mu, dens(xs), dens(xs), tg)
+    assert np.abs(pb - pe).max() <= 1e-13 * np.abs(pe).max()
+
+
+def test_offsurface_near_correction_recovers_integral(oracle_mod):
+    """Targets 0.1-0.6 from sphere 0's surface, band-limited densities on two
+    spheres: smooth sum + near correction == converged quadrature, for u and p
+    (eta = 5 so that sphere 1 is corrected too: at p = 8 the smooth rule alone
+    is only ~1e-9 accurate even two radii away); the plain smooth sum is far off."""
+    p, mu = 8, 1.2
+    c = np.array([[0.0, 0.0, 0.0], [3.5, 0.4, -0.3]])
+    a = np.array([1.0, 0.8])
+    x, _, _ = oracle_mod.nodes(c, a, p)
+    ns = (p + 1) * (2 * p + 2)
+    mods = [(1, 0, 0), (2, 1, 1), (3, -2, 2), (4, 3, 1)]
+    g = np.zeros((2 * ns, 3))
+    g[:ns] = sum(H.vsh_density(n, m, ch, x[:ns], c[0], a[0]) for n, m, ch in mods)
+    g[ns:] = sum(H.vsh_density(n, m, ch, x[ns:], c[1], a[1]) for n, m, ch in mods[:2])
+    d = _dirs(9, 16)
+    tg = c[0] + d * (1.0 + np.random.default_rng(10).uniform(0.1, 0.6, (16, 1)))
+    u, pr = oracle_mod.offsurface_near(c, a, p, mu, g, g, 5.0, tg)
+    u0, p0 = oracle_mod.offsurface(c, a, p, mu, g, g, tg)
+    xs, _, _ = oracle_mod.nodes(c, a, 160)   # p_src = 96 is still 3e-12 off at gap 0.1
+    nb = 161 * 322
+    gs = np.zeros((2 * nb, 3))
+    gs[:nb] = sum(H.vsh_density(n, m, ch, xs[:nb], c[0], a[0]) for n, m, ch in mods)
+    gs[nb:] = sum(H.vsh_density(n, m, ch, xs[nb:], c[1], a[1]) for n, m, ch in mods[:2])
+    ur, prr = oracle_mod.offsurface(c, a, 96, mu, gs, gs, tg)
+    assert np.abs(u - ur).max() <= 1e-13 * np.abs(ur).max()
+    assert np.abs(pr - prr).max() <= 1e-13 * np.abs(prr).max()
+    assert np.abs(u0 - ur).max() >= 1e-4 * np.abs(ur).max()
