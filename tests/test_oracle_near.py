@@ -191,7 +191,7 @@ def test_offsurface_near_correction_recovers_integral(oracle_mod):
     gs = np.zeros((2 * nb, 3))
     gs[:nb] = sum(H.vsh_density(n, m, ch, xs[:nb], c[0], a[0]) for n, m, ch in mods)
     gs[nb:] = sum(H.vsh_density(n, m, ch, xs[nb:], c[1], a[1]) for n, m, ch in mods[:2])
-    ur, prr = oracle_mod.offsurface(c, a, 96, mu, gs, gs, tg)
+    ur, prr = oracle_mod.offsurface(c, a, 160, mu, gs, gs, tg)
     assert np.abs(u - ur).max() <= 1e-13 * np.abs(ur).max()
     assert np.abs(pr - prr).max() <= 1e-13 * np.abs(prr).max()
     assert np.abs(u0 - ur).max() >= 1e-4 * np.abs(ur).max()
