@@ -190,9 +190,12 @@ int bie_reset_profile(bie_ctx* ctx);
  * exterior field of the source sphere's degree-<=p vector spherical harmonic
  * expansion (eqs 3.6-3.11 with reading R1, eq 4.7; the expansion is the
  * discrete projection of reading R9).  eta = 0 disables it (the default, and
- * the BASELINE.json metric path).  Builds the neighbour lists on the device
- * and synchronises.  BIE_ERR_ARG for eta < 0 or non-finite.
- * The off-surface evaluator is not affected.
+ * the BASELINE.json metric path).  bie_eval_offsurface applies the same
+ * correction to u and p at every target x within eta * 2 a_s of the surface
+ * of a sphere s (|x - c_s| - a_s < eta * 2 a_s, SPEC's point-to-surface form
+ * of eq 4.5), using the exterior pressures of P:189 (S) and reading R12 (D).
+ * Builds the neighbour lists on the device and synchronises.  BIE_ERR_ARG for
+ * eta < 0 or non-finite.
  */
 int bie_set_near(bie_ctx* ctx, double eta);
 

@@ -66,6 +66,7 @@ struct bie_ctx {
   int* d_nb_idx = nullptr;
   int* d_near_tgt = nullptr;
   double* d_alpha = nullptr;
+  double* d_ncoef = nullptr;
   // staging for the _host entry points
   double *d_f = nullptr, *d_q = nullptr, *d_u = nullptr;
   double *d_tg = nullptr, *d_uo = nullptr, *d_po = nullptr;
@@ -248,6 +249,18 @@ static int launch_check(bie_ctx* c, const char* what) {
 
 static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode = 0);
 
+// per-sphere exterior-expansion coefficients from the k_self projections
+static int run_near_coef(bie_ctx* c, cudaStream_t s) {
+  const TableLayout L(c->p);
+  const int64_t n = c->ns * L.nlm;
+  Ev ev;
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  k_near_coef<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(c->p, c->ns, c->mu, c->d_radii, c->d_alpha,
+                                                          c->d_ncoef);
+  prof_end(c, s, &ev);
+  return launch_check(c, "k_near_coef");
+}
+
 static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
                      cudaStream_t s) {
   // rows a2 + a4-a6: self term (or zeros) into u, packed sources into d_rec
@@ -273,18 +286,21 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   int rc = launch_check(c, "k_self");
   if (rc) return rc;
   if (!(parts & BIE_PART_FAR)) return BIE_OK;
+  if (near) {
+    rc = run_near_coef(c, s);
+    if (rc) return rc;
+  }
   rc = run_far(c, u, s);
   if (rc || !near) return rc;
   // NEXT-1: replace the smooth rule by the exterior expansion for near pairs
   NearArgs NA;
   NA.p = c->p;
   NA.nsn = c->nsn;
-  NA.mu = c->mu;
   NA.tab = c->d_tab;
   NA.centres = c->d_centres;
   NA.radii = c->d_radii;
   NA.rec = c->d_rec;
-  NA.alpha = c->d_alpha;
+  NA.coef = c->d_ncoef;
   NA.tgt = c->d_near_tgt;
   NA.nb_off = c->d_nb_off;
   NA.nb_idx = c->d_nb_idx;
@@ -344,11 +360,33 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
                           int64_t m, double* u, double* p, cudaStream_t s) {
   if (m == 0) return BIE_OK;
   Ev ev;
+  const bool near = c->eta > 0.0 && c->d_alpha;
+  int rc;
+  if (near) {  // NEXT-1 at targets: VSH projections of every sphere, then coefficients
+    SelfArgs SA;
+    SA.p = c->p;
+    SA.ns = c->ns;
+    SA.mu = c->mu;
+    SA.tab = c->d_tab;
+    SA.centres = c->d_centres;
+    SA.radii = c->d_radii;
+    SA.f = f;
+    SA.q = q;
+    SA.u = nullptr;
+    SA.rec = c->d_rec;
+    SA.self = 0;
+    SA.alpha = c->d_alpha;
+    prof_begin(c, BIE_KIND_SELF, s, &ev);
+    k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_self"))) return rc;
+    if ((rc = run_near_coef(c, s))) return rc;
+  }
   prof_begin(c, BIE_KIND_PACK, s, &ev);
   k_pack<<<(unsigned)((c->N + 255) / 256), 256, 0, s>>>(c->p, c->N, c->mu, c->d_tab, c->d_centres,
                                                         c->d_radii, f, q, c->d_rec, c->d_qn3);
   prof_end(c, s, &ev);
-  int rc = launch_check(c, "k_pack");
+  rc = launch_check(c, "k_pack");
   if (rc) return rc;
   const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
   for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
@@ -392,7 +430,29 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
     rc = launch_check(c, "k_reduce");
     if (rc) return rc;
   }
-  return BIE_OK;
+  if (!near) return BIE_OK;
+  NearOffArgs NO;
+  NO.p = c->p;
+  NO.nsn = c->nsn;
+  NO.ns = c->ns;
+  NO.M = m;
+  NO.mu = c->mu;
+  NO.eta = c->eta;
+  NO.tab = c->d_tab;
+  NO.centres = c->d_centres;
+  NO.radii = c->d_radii;
+  NO.rec = c->d_rec;
+  NO.qn3 = c->d_qn3;
+  NO.coef = c->d_ncoef;
+  NO.tx = tg;
+  NO.u = u;
+  NO.pres = p;
+  const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  if (p) k_near_off<true><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
+  else k_near_off<false><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
+  prof_end(c, s, &ev);
+  return launch_check(c, "k_near_off");
 }
 
 // ================================================================ ABI
@@ -423,6 +483,7 @@ void bie_destroy(bie_ctx* c) {
   for (int* p : iptrs)
     if (p) cudaFree(p);
   if (c->d_alpha) cudaFree(c->d_alpha);
+  if (c->d_ncoef) cudaFree(c->d_ncoef);
   delete c;
 }
 
@@ -490,6 +551,10 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   cudaFuncSetAttribute(k_self, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_near, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p) * sizeof(double)));
+  cudaFuncSetAttribute(k_near_off<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_off_smem_doubles(p) * sizeof(double)));
+  cudaFuncSetAttribute(k_near_off<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_off_smem_doubles(p) * sizeof(double)));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
@@ -721,8 +786,9 @@ static void near_free(bie_ctx* c) {
   cudaFree(c->d_nb_idx);
   cudaFree(c->d_near_tgt);
   cudaFree(c->d_alpha);
+  cudaFree(c->d_ncoef);
   c->d_nb_off = c->d_nb_idx = c->d_near_tgt = nullptr;
-  c->d_alpha = nullptr;
+  c->d_alpha = c->d_ncoef = nullptr;
   c->n_near_tgt = 0;
   c->n_near_pairs = 0;
 }
@@ -756,11 +822,16 @@ int bie_set_near(bie_ctx* c, double eta) {
   c->n_near_pairs = off[ns];
   c->n_near_tgt = (int)tgt.size();
   cudaFree(d_cnt);
-  if (c->n_near_pairs == 0) return launch_check(c, "k_near_lists");
   const TableLayout L(c->p);
+  if (cudaMalloc(&c->d_alpha, (size_t)ns * 12 * L.nlm * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->d_ncoef, (size_t)ns * 10 * L.nlm * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    near_free(c);
+    return fail(c, BIE_ERR_ALLOC, "near coefficients%s");
+  }
+  if (c->n_near_pairs == 0) return launch_check(c, "k_near_lists");
   if (cudaMalloc(&c->d_nb_idx, off[ns] * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&c->d_near_tgt, tgt.size() * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&c->d_alpha, (size_t)ns * 12 * L.nlm * sizeof(double)) != cudaSuccess) {
+      cudaMalloc(&c->d_near_tgt, tgt.size() * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     near_free(c);
     return fail(c, BIE_ERR_ALLOC, "near lists%s");

@@ -48,12 +48,11 @@ __global__ void k_near_lists(int64_t ns, const double* __restrict__ centres,
 
 struct NearArgs {
   int p, nsn;
-  double mu;
   const double* tab;
   const double* centres;
   const double* radii;
   const double* rec;     // packed sources (x, n, f', q') of all nodes
-  const double* alpha;   // [ns][2][nlm][3][2] from k_self
+  const double* coef;    // [ns][nlm][10] from k_near_coef
   const int* tgt;        // target spheres with >= 1 near neighbour
   const int* nb_off;     // [ns+1]
   const int* nb_idx;     // neighbour sphere indices
@@ -62,140 +61,41 @@ struct NearArgs {
 
 __host__ __device__ inline int64_t near_smem_doubles(int p) {
   const int nlm = (p + 1) * (p + 2) / 2, nsn = (p + 1) * (2 * p + 2);
-  return 8LL * nlm + 3LL * nsn + 3LL * nlm;
+  return 3LL * nsn + 3LL * nlm;
 }
 
+template <bool PRESSURE>
+__device__ __forceinline__ void exterior_field(int p, const double* __restrict__ cf,
+                                               const double* rA, const double* rB,
+                                               const double* rC, const double* c, double a,
+                                               const double* x, double ex[3], double* pex);
+
+// One CTA per target sphere t with near neighbours; for each neighbour s (in
+// ascending index) every thread adds exterior_s(x) - smooth_s(x) at its nodes.
 __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, nsn = A.nsn;
   const TableLayout L(p);
   const int nlm = L.nlm;
-  double* cf = sm;              // [nlm][c1,c2,c3,c4][re,im]
-  double* du = cf + 8 * nlm;    // [nsn][3]
+  double* du = sm;              // [nsn][3]
   double* rt = du + 3 * nsn;    // rA, rB, rC [3][nlm]
   const int tid = threadIdx.x, nt = blockDim.x;
   const int t = A.tgt[blockIdx.x];
   for (int e = tid; e < 3 * nlm; e += nt) rt[e] = A.tab[L.rA + e];
   for (int e = tid; e < 3 * nsn; e += nt) du[e] = 0.0;
-  const double* rA = rt;
-  const double* rB = rt + nlm;
-  const double* rC = rt + 2 * nlm;
-  const double inv_sqrt4pi = 0.28209479177387814347;
-
+  __syncthreads();
   for (int qn = A.nb_off[t]; qn < A.nb_off[t + 1]; ++qn) {
     const int s = A.nb_idx[qn];
-    __syncthreads();  // previous source's coefficients no longer in use
-    // exterior-formula coefficients of source sphere s (eqs 3.6-3.11):
-    //   beta_V = c1 r^{-n-2} + c2 r^{-n},  beta_W = c3 r^{-n},  beta_X = c4 r^{-n-1}
-    for (int c = tid; c < nlm; c += nt) {
-      int m = 0, off = 0;
-      while (off + (p + 1 - m) <= c) { off += p + 1 - m; ++m; }
-      const int n = m + (c - off);
-      const double* af = A.alpha + ((int64_t)s * 2 * nlm + c) * 6;
-      const double* aq = A.alpha + ((int64_t)s * 2 * nlm + nlm + c) * 6;
-      const double inn = n ? 1.0 / ((double)n * (n + 1)) : 0.0;
-      const double i2n = 1.0 / (2.0 * n + 1.0);
-      const double lSV = n / ((2.0 * n + 1.0) * (2.0 * n + 3.0));
-      const double lDV = (2.0 * n * n + 4.0 * n + 3.0) / ((2.0 * n + 1.0) * (2.0 * n + 3.0));
-      const double xS = n / (4.0 * n + 2.0), xD = 2.0 * n * (n - 1.0) / (4.0 * n + 2.0);
-      const double wS = n ? (n + 1.0) / ((2.0 * n + 1.0) * (2.0 * n - 1.0)) : 0.0;
-      const double wD = n ? 2.0 * (n + 1.0) * (n - 1.0) / ((2.0 * n + 1.0) * (2.0 * n - 1.0)) : 0.0;
-      const double kS = n ? 1.0 / (2.0 * n + 1.0) : 0.0, kD = n ? (n - 1.0) / (2.0 * n + 1.0) : 0.0;
-      double* o = cf + 8 * c;
-#pragma unroll
-      for (int ri = 0; ri < 2; ++ri) {
-        const double fV = (n * af[2 + ri] * inn - af[ri]) * i2n;
-        const double fW = n ? ((n + 1) * af[2 + ri] * inn + af[ri]) * i2n : 0.0;
-        const double fX = af[4 + ri] * inn;
-        const double qV = (n * aq[2 + ri] * inn - aq[ri]) * i2n;
-        const double qW = n ? ((n + 1) * aq[2 + ri] * inn + aq[ri]) * i2n : 0.0;
-        const double qX = aq[4 + ri] * inn;
-        o[0 + ri] = fV * lSV + fW * xS + qV * lDV + qW * xD;  // c1
-        o[2 + ri] = -(fW * xS + qW * xD);                     // c2
-        o[4 + ri] = fW * wS + qW * wD;                        // c3
-        o[6 + ri] = fX * kS + qX * kD;                        // c4
-      }
-    }
-    __syncthreads();
+    const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
     const double a = A.radii[s];
-    const double csx = A.centres[3 * s], csy = A.centres[3 * s + 1], csz = A.centres[3 * s + 2];
+    const double* cf = A.coef + (int64_t)s * nlm * 10;
+    const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
     for (int kk = tid; kk < nsn; kk += nt) {
       const int64_t i = (int64_t)t * nsn + kk;
       const double xt[3] = {A.rec[i * kRec], A.rec[i * kRec + 1], A.rec[i * kRec + 2]};
-      // ---- exterior field of s at x (spherical frame of s)
-      const double r0 = (xt[0] - csx) / a, r1 = (xt[1] - csy) / a, r2v = (xt[2] - csz) / a;
-      const double rxy = sqrt(r0 * r0 + r1 * r1);
-      const double r = sqrt(rxy * rxy + r2v * r2v);
-      const double rho = 1.0 / r;
-      const double ct = r2v * rho, st = rxy * rho;
-      const double cp = rxy > 0.0 ? r0 / rxy : 1.0, sp = rxy > 0.0 ? r1 / rxy : 0.0;
-      double ur = 0.0, uth = 0.0, uph = 0.0;
-      double e_re = 1.0, e_im = 0.0;  // e^{i m phi}
-      double rho_m = 1.0;             // rho^m
-      double pbar_mm = 0.0;           // P~_m^m / sin(theta), m >= 1
-      for (int m = 0; m <= p; ++m) {
-        double Ur0 = 0, Ur1 = 0, Ut0 = 0, Ut1 = 0, Up0 = 0, Up1 = 0;
-        double Pp = 0.0, Pc, dPp = 0.0, dPc = 0.0;  // m = 0: P~ and dP~/dtheta chains
-        if (m == 0) {
-          Pc = inv_sqrt4pi;
-        } else {
-          pbar_mm = (m == 1) ? inv_sqrt4pi * sqrt(1.5) : pbar_mm * st * sqrt((2.0 * m + 1.0) / (2.0 * m));
-          Pc = pbar_mm;  // m >= 1: chain of P~ / sin(theta)
-        }
-        double rn = rho_m;
-        const int c0 = lm_index(p, m, m);
-        for (int n = m; n <= p; ++n) {
-          const int c = c0 + (n - m);
-          if (n > m) {
-            const double nx = rA[c] * (ct * Pc - rB[c] * Pp);
-            if (m == 0) {
-              const double dnx = rA[c] * (ct * dPc - st * Pc - rB[c] * dPp);
-              dPp = dPc;
-              dPc = dnx;
-            }
-            Pp = Pc;
-            Pc = nx;
-          }
-          double Pt, dPt, mPs;
-          if (m == 0) {
-            Pt = Pc;
-            dPt = dPc;
-            mPs = 0.0;
-          } else {
-            Pt = st * Pc;
-            mPs = m * Pc;
-            dPt = n * ct * Pc - rC[c] * (n > m ? Pp : 0.0);
-          }
-          const double* o = cf + 8 * c;
-          const double bV0 = rn * fma(o[0], rho * rho, o[2]), bV1 = rn * fma(o[1], rho * rho, o[3]);
-          const double bW0 = rn * o[4], bW1 = rn * o[5];
-          const double bX0 = rn * rho * o[6], bX1 = rn * rho * o[7];
-          const double gG0 = bV0 + bW0, gG1 = bV1 + bW1;                          // psi^G
-          const double gY0 = -(n + 1.0) * bV0 + n * bW0, gY1 = -(n + 1.0) * bV1 + n * bW1;  // psi^Y
-          Ur0 = fma(gY0, Pt, Ur0);
-          Ur1 = fma(gY1, Pt, Ur1);
-          Ut0 = fma(gG0, dPt, fma(bX1, mPs, Ut0));   // psiG dP - i psiX mP
-          Ut1 = fma(gG1, dPt, fma(-bX0, mPs, Ut1));
-          Up0 = fma(bX0, dPt, fma(-gG1, mPs, Up0));  // i psiG mP + psiX dP
-          Up1 = fma(bX1, dPt, fma(gG0, mPs, Up1));
-          rn *= rho;
-        }
-        const double wm = m ? 2.0 : 1.0;
-        ur += wm * (Ur0 * e_re - Ur1 * e_im);
-        uth += wm * (Ut0 * e_re - Ut1 * e_im);
-        uph += wm * (Up0 * e_re - Up1 * e_im);
-        const double ne = e_re * cp - e_im * sp;
-        e_im = e_re * sp + e_im * cp;
-        e_re = ne;
-        rho_m *= rho;
-      }
       double ex[3];
-      ex[0] = ur * st * cp + uth * ct * cp - uph * sp;
-      ex[1] = ur * st * sp + uth * ct * sp + uph * cp;
-      ex[2] = ur * ct - uth * st;
-      // ---- smooth-rule contribution of s at x (same pair formula as k_nbody)
+      exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
       double acc[3] = {0.0, 0.0, 0.0}, pdummy = 0.0;
-      const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
       for (int k = 0; k < nsn; ++k) {
         const double2* q2 = sr + k * (kRec / 2);
         pair_acc<false, false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3), __ldg(q2 + 4),
@@ -208,6 +108,236 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   }
   __syncthreads();
   for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
+}
+
+}  // namespace bie
+
+namespace bie {
+
+// ------------------------------------------- per-sphere expansion coefficients
+// coef[s][c][0..9]: c1, c2, c3, c4 (velocity, as in k_near) and cp (pressure)
+// for sphere s and (n, m) column c, complex (re, im):
+//   beta_V = c1 r^{-n-2} + c2 r^{-n}, beta_W = c3 r^{-n}, beta_X = c4 r^{-n-1},
+//   p = sum cp Y_n^m r^{-n-1},  cp = (mu/a) [n aW_f + 2n(n-1) aW_q]
+// (P:189 and reading R12 for the exterior pressures; R5/R6 scalings).
+__global__ void k_near_coef(int p, int64_t ns, double mu, const double* __restrict__ radii,
+                            const double* __restrict__ alpha, double* __restrict__ coef) {
+  const TableLayout L(p);
+  const int nlm = L.nlm;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ns * nlm) return;
+  const int64_t s = e / nlm;
+  const int c = (int)(e - s * nlm);
+  int m = 0, off = 0;
+  while (off + (p + 1 - m) <= c) { off += p + 1 - m; ++m; }
+  const int n = m + (c - off);
+  const double* af = alpha + ((int64_t)s * 2 * nlm + c) * 6;
+  const double* aq = alpha + ((int64_t)s * 2 * nlm + nlm + c) * 6;
+  const double inn = n ? 1.0 / ((double)n * (n + 1)) : 0.0;
+  const double i2n = 1.0 / (2.0 * n + 1.0);
+  const double lSV = n / ((2.0 * n + 1.0) * (2.0 * n + 3.0));
+  const double lDV = (2.0 * n * n + 4.0 * n + 3.0) / ((2.0 * n + 1.0) * (2.0 * n + 3.0));
+  const double xS = n / (4.0 * n + 2.0), xD = 2.0 * n * (n - 1.0) / (4.0 * n + 2.0);
+  const double wS = n ? (n + 1.0) / ((2.0 * n + 1.0) * (2.0 * n - 1.0)) : 0.0;
+  const double wD = n ? 2.0 * (n + 1.0) * (n - 1.0) / ((2.0 * n + 1.0) * (2.0 * n - 1.0)) : 0.0;
+  const double kS = n ? 1.0 / (2.0 * n + 1.0) : 0.0, kD = n ? (n - 1.0) / (2.0 * n + 1.0) : 0.0;
+  const double pm = mu / radii[s];
+  double* o = coef + e * 10;
+#pragma unroll
+  for (int ri = 0; ri < 2; ++ri) {
+    const double fV = (n * af[2 + ri] * inn - af[ri]) * i2n;
+    const double fW = n ? ((n + 1) * af[2 + ri] * inn + af[ri]) * i2n : 0.0;
+    const double fX = af[4 + ri] * inn;
+    const double qV = (n * aq[2 + ri] * inn - aq[ri]) * i2n;
+    const double qW = n ? ((n + 1) * aq[2 + ri] * inn + aq[ri]) * i2n : 0.0;
+    const double qX = aq[4 + ri] * inn;
+    o[0 + ri] = fV * lSV + fW * xS + qV * lDV + qW * xD;
+    o[2 + ri] = -(fW * xS + qW * xD);
+    o[4 + ri] = fW * wS + qW * wD;
+    o[6 + ri] = fX * kS + qX * kD;
+    o[8 + ri] = pm * (n * fW + 2.0 * n * (n - 1.0) * qW);
+  }
+}
+
+// Exterior velocity (and pressure) of sphere (c, a) with coefficient block cf
+// at point x: the expansion of eq 4.7 with eqs 3.6-3.11 (same algebra as k_near).
+template <bool PRESSURE>
+__device__ __forceinline__ void exterior_field(int p, const double* __restrict__ cf,
+                                               const double* rA, const double* rB,
+                                               const double* rC, const double* c, double a,
+                                               const double* x, double ex[3], double* pex) {
+  const double r0 = (x[0] - c[0]) / a, r1 = (x[1] - c[1]) / a, r2v = (x[2] - c[2]) / a;
+  const double rxy = sqrt(r0 * r0 + r1 * r1);
+  const double r = sqrt(rxy * rxy + r2v * r2v);
+  const double rho = 1.0 / r;
+  const double ct = r2v * rho, st = rxy * rho;
+  const double cp = rxy > 0.0 ? r0 / rxy : 1.0, sp = rxy > 0.0 ? r1 / rxy : 0.0;
+  const double inv_sqrt4pi = 0.28209479177387814347;
+  double ur = 0.0, uth = 0.0, uph = 0.0, pr = 0.0;
+  double e_re = 1.0, e_im = 0.0, rho_m = 1.0, pbar_mm = 0.0;
+  for (int m = 0; m <= p; ++m) {
+    double Ur0 = 0, Ur1 = 0, Ut0 = 0, Ut1 = 0, Up0 = 0, Up1 = 0, Pp0 = 0, Pp1 = 0;
+    double Pp = 0.0, Pc, dPp = 0.0, dPc = 0.0;
+    if (m == 0) {
+      Pc = inv_sqrt4pi;
+    } else {
+      pbar_mm = (m == 1) ? inv_sqrt4pi * sqrt(1.5) : pbar_mm * st * sqrt((2.0 * m + 1.0) / (2.0 * m));
+      Pc = pbar_mm;
+    }
+    double rn = rho_m;
+    const int c0 = lm_index(p, m, m);
+    for (int n = m; n <= p; ++n) {
+      const int cc = c0 + (n - m);
+      if (n > m) {
+        const double nx = rA[cc] * (ct * Pc - rB[cc] * Pp);
+        if (m == 0) {
+          const double dnx = rA[cc] * (ct * dPc - st * Pc - rB[cc] * dPp);
+          dPp = dPc;
+          dPc = dnx;
+        }
+        Pp = Pc;
+        Pc = nx;
+      }
+      double Pt, dPt, mPs;
+      if (m == 0) {
+        Pt = Pc;
+        dPt = dPc;
+        mPs = 0.0;
+      } else {
+        Pt = st * Pc;
+        mPs = m * Pc;
+        dPt = n * ct * Pc - rC[cc] * (n > m ? Pp : 0.0);
+      }
+      const double* o = cf + 10 * cc;
+      const double bV0 = rn * fma(o[0], rho * rho, o[2]), bV1 = rn * fma(o[1], rho * rho, o[3]);
+      const double bW0 = rn * o[4], bW1 = rn * o[5];
+      const double bX0 = rn * rho * o[6], bX1 = rn * rho * o[7];
+      const double gG0 = bV0 + bW0, gG1 = bV1 + bW1;
+      const double gY0 = -(n + 1.0) * bV0 + n * bW0, gY1 = -(n + 1.0) * bV1 + n * bW1;
+      Ur0 = fma(gY0, Pt, Ur0);
+      Ur1 = fma(gY1, Pt, Ur1);
+      Ut0 = fma(gG0, dPt, fma(bX1, mPs, Ut0));
+      Ut1 = fma(gG1, dPt, fma(-bX0, mPs, Ut1));
+      Up0 = fma(bX0, dPt, fma(-gG1, mPs, Up0));
+      Up1 = fma(bX1, dPt, fma(gG0, mPs, Up1));
+      if (PRESSURE) {
+        Pp0 = fma(o[8] * rn * rho, Pt, Pp0);
+        Pp1 = fma(o[9] * rn * rho, Pt, Pp1);
+      }
+      rn *= rho;
+    }
+    const double wm = m ? 2.0 : 1.0;
+    ur += wm * (Ur0 * e_re - Ur1 * e_im);
+    uth += wm * (Ut0 * e_re - Ut1 * e_im);
+    uph += wm * (Up0 * e_re - Up1 * e_im);
+    if (PRESSURE) pr += wm * (Pp0 * e_re - Pp1 * e_im);
+    const double ne = e_re * cp - e_im * sp;
+    e_im = e_re * sp + e_im * cp;
+    e_re = ne;
+    rho_m *= rho;
+  }
+  ex[0] = ur * st * cp + uth * ct * cp - uph * sp;
+  ex[1] = ur * st * sp + uth * ct * sp + uph * cp;
+  ex[2] = ur * ct - uth * st;
+  if (PRESSURE) *pex = pr;
+}
+
+// ------------------------------------------- near correction at arbitrary targets
+// One thread per target.  Near spheres (point-to-surface form of eq 4.5:
+// |x - c_s| - a_s < eta 2 a_s) are found by scanning the sphere list through
+// shared-memory tiles in ascending index, up to kNearList at a time, then each
+// is evaluated (exterior expansion minus smooth rule) -- all lanes run the same
+// code on different spheres, so the warp stays convergent.  u[t] += du,
+// p[t] += dp after the smooth-sum kernels (deterministic).
+constexpr int kNearList = 16;
+constexpr int kSphTile = 256;
+
+struct NearOffArgs {
+  int p, nsn;
+  int64_t ns, M;
+  double mu, eta;
+  const double* tab;
+  const double* centres;
+  const double* radii;
+  const double* rec;
+  const double* qn3;
+  const double* coef;  // [ns][nlm][10]
+  const double* tx;    // [M][3]
+  double* u;           // [M][3] accumulated
+  double* pres;        // [M] accumulated, nullable
+};
+
+__host__ __device__ inline int64_t near_off_smem_doubles(int p) {
+  const int nlm = (p + 1) * (p + 2) / 2;
+  return 3LL * nlm + 4LL * kSphTile;
+}
+
+template <bool PRESSURE>
+__global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
+  extern __shared__ __align__(16) double sm[];
+  const int p = A.p, nsn = A.nsn;
+  const TableLayout L(p);
+  const int nlm = L.nlm;
+  double* rt = sm;                // rA, rB, rC
+  double* tile = sm + 3 * nlm;    // [kSphTile][4]: centre, radius
+  for (int e = threadIdx.x; e < 3 * nlm; e += blockDim.x) rt[e] = A.tab[L.rA + e];
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = t < A.M;
+  const int64_t tc = live ? t : A.M - 1;
+  const double x[3] = {A.tx[3 * tc], A.tx[3 * tc + 1], A.tx[3 * tc + 2]};
+  double du[3] = {0.0, 0.0, 0.0}, dp = 0.0;
+  int list[kNearList];
+  int cnt = 0;
+  auto flush = [&]() {
+    for (int j = 0; j < cnt; ++j) {
+      const int s = list[j];
+      const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+      double ex[3], pe = 0.0;
+      exterior_field<PRESSURE>(p, A.coef + (int64_t)s * nlm * 10, rt, rt + nlm, rt + 2 * nlm, cs,
+                               A.radii[s], x, ex, &pe);
+      double acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
+      const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
+      const double* sq = A.qn3 + (int64_t)s * nsn;
+      for (int k = 0; k < nsn; ++k) {
+        const double2* q2 = sr + k * (kRec / 2);
+        pair_acc<false, PRESSURE>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3),
+                                  __ldg(q2 + 4), __ldg(q2 + 5), PRESSURE ? __ldg(sq + k) : 0.0, x,
+                                  acc, pacc, 0, 0, 1);
+      }
+      du[0] += ex[0] - acc[0];
+      du[1] += ex[1] - acc[1];
+      du[2] += ex[2] - acc[2];
+      if (PRESSURE) dp += pe - 2.0 * A.mu * pacc;
+    }
+    cnt = 0;
+  };
+  for (int64_t s0 = 0; s0 < A.ns; s0 += kSphTile) {
+    const int nt = (int)min((int64_t)kSphTile, A.ns - s0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt; e += blockDim.x) {
+      tile[4 * e] = A.centres[3 * (s0 + e)];
+      tile[4 * e + 1] = A.centres[3 * (s0 + e) + 1];
+      tile[4 * e + 2] = A.centres[3 * (s0 + e) + 2];
+      tile[4 * e + 3] = A.radii[s0 + e];
+    }
+    __syncthreads();
+    for (int e = 0; e < nt; ++e) {
+      const double dx = __dsub_rn(x[0], tile[4 * e]), dy = __dsub_rn(x[1], tile[4 * e + 1]),
+                   dz = __dsub_rn(x[2], tile[4 * e + 2]);
+      const double a = tile[4 * e + 3];
+      const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+      if (live && __dsub_rn(r, a) < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {
+        list[cnt++] = (int)(s0 + e);
+        if (cnt == kNearList) flush();
+      }
+    }
+  }
+  flush();
+  if (!live) return;
+  A.u[3 * t] += du[0];
+  A.u[3 * t + 1] += du[1];
+  A.u[3 * t + 2] += du[2];
+  if (PRESSURE && A.pres) A.pres[t] += dp;
 }
 
 }  // namespace bie

@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
     }
   }
   if (!A.self && !A.alpha) {
-    for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
+    if (A.u)
+      for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
     return;
   }
   __syncthreads();
@@ -167,7 +168,8 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
     }
   }
   if (!A.self) {
-    for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
+    if (A.u)
+      for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
     return;
   }
   __syncthreads();

@@ -117,3 +117,53 @@ def test_near_config4_subset(bie, oracle_mod):
     assert npairs > 0
     ref = oracle_mod.apply_near(d["centres"], d["radii"], d["p"], d["mu"], f, q, 1.0, sub)
     _assert_parity(got[sub], ref, "cfg4 near")
+
+
+# ------------------------------------------------- off-surface targets (a7)
+def _near_targets(c, a, n, seed, lo=0.1, hi=1.5):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        s = rng.integers(len(a))
+        d = rng.standard_normal(3)
+        x = c[s] + d / np.linalg.norm(d) * a[s] * (1.0 + rng.uniform(lo, hi))
+        if np.all(np.linalg.norm(x - c, axis=1) - a > 0.05):
+            out.append(x)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("p,ns,eta,use_p", [(5, 4, 1.0, True), (8, 6, 0.5, True), (6, 3, 2.0, False)])
+def test_offsurface_near_matches_oracle(bie, oracle_mod, p, ns, eta, use_p):
+    c, a, f, q, mu = _random_case(900 + p, ns, p, True, 1.4)
+    tg = _near_targets(c, a, 300, p)
+    uref, pref = oracle_mod.offsurface_near(c, a, p, mu, f, q, eta, tg)
+    ctx = bie.bie_create(c, a, p, mu)
+    bie.bie_set_near(ctx, eta)
+    u = torch.empty((len(tg), 3), dtype=torch.float64, device="cuda")
+    pr = torch.empty(len(tg), dtype=torch.float64, device="cuda") if use_p else None
+    bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), _dev(tg), u, pr)
+    torch.cuda.synchronize()
+    ctx.close()
+    _assert_parity(u.cpu().numpy(), uref, "offsurface near u")
+    if use_p:
+        _assert_parity(pr.cpu().numpy(), pref, "offsurface near p")
+
+
+def test_offsurface_near_config5_subset(bie, oracle_mod):
+    """cfg 5 (targets >= 0.25 from every surface) with eta = 1."""
+    from tests.test_gpu_parity import _cfg_inputs
+    d, f, q = _cfg_inputs(oracle_mod, 5)
+    tsub = d["target_subset"][::16]
+    ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
+    bie.bie_set_near(ctx, 1.0)
+    tg = _dev(d["targets"])
+    M = tg.shape[0]
+    u = torch.empty((M, 3), dtype=torch.float64, device="cuda")
+    pr = torch.empty(M, dtype=torch.float64, device="cuda")
+    bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), tg, u, pr)
+    torch.cuda.synchronize()
+    ctx.close()
+    uref, pref = oracle_mod.offsurface_near(d["centres"], d["radii"], d["p"], d["mu"], f, q, 1.0,
+                                            d["targets"][tsub])
+    _assert_parity(u.cpu().numpy()[tsub], uref, "cfg5 near u")
+    _assert_parity(pr.cpu().numpy()[tsub], pref, "cfg5 near p")
