@@ -221,9 +221,14 @@ int64_t bie_near_pairs(const bie_ctx* ctx);
  *   (restart + 2) x 3N doubles is allocated per call.
  *   The force on sphere s is -sum_{k in s} w_k mu_k (Stokes drag; pinned in
  *   tests/test_oracle_porous.py).
+ *   precond = 1: right preconditioning by the exact inverse of each sphere's
+ *   own operator P = 1/2 I + S_self + D_self, which the spectra of Thm 2 make
+ *   diagonal in the VSH basis (eigenvalue 1/(1/2 + lamS a/mu + lamD_pv) on
+ *   every mode of degree <= p, 2 on the remainder); applied by the self-term
+ *   kernel.  precond = 0: plain GMRES.
  */
 int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, int max_iter,
-                     int restart, int* iters, double* rel_resid, bie_stream_t s);
+                     int restart, int precond, int* iters, double* rel_resid, bie_stream_t s);
 
 /*
  * Tuning knob: number of source chunks of the far-field kernel (0 = automatic;

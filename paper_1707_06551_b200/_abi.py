@@ -57,7 +57,7 @@ _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
 _lib.bie_near_pairs.restype = _i64
 _lib.bie_apply_K.argtypes = [_vp, _vp, _vp, _i32, _vp]
-_lib.bie_solve_porous.argtypes = [_vp, _vp, _vp, _d, _i32, _i32, ctypes.POINTER(_i32),
+_lib.bie_solve_porous.argtypes = [_vp, _vp, _vp, _d, _i32, _i32, _i32, ctypes.POINTER(_i32),
                                   ctypes.POINTER(_d), _vp]
 _lib.bie_status_string.argtypes = [_i32]
 _lib.bie_status_string.restype = ctypes.c_char_p
@@ -268,13 +268,14 @@ def bie_near_pairs(ctx) -> int:
     return int(_lib.bie_near_pairs(ctx.handle))
 
 
-def bie_solve_porous(ctx, uinf, mu, tol=1e-12, max_iter=200, restart=50, stream=None):
+def bie_solve_porous(ctx, uinf, mu, tol=1e-12, max_iter=200, restart=50, precond=True, stream=None):
     """GMRES solve of BIE 5.4; returns (iterations, true relative residual)."""
     N = bie_num_nodes(ctx)
     it, res = ctypes.c_int(), ctypes.c_double()
     _check(ctx, _lib.bie_solve_porous(ctx.handle, _ptr(uinf, device=True, n=3 * N),
                                       _ptr(mu, device=True, n=3 * N), float(tol), int(max_iter),
-                                      int(restart), ctypes.byref(it), ctypes.byref(res),
+                                      int(restart), int(bool(precond)), ctypes.byref(it),
+                                      ctypes.byref(res),
                                       _stream(stream)))
     return it.value, res.value
 

@@ -278,6 +278,7 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
   const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
   SA.alpha = near ? c->d_alpha : nullptr;
+  SA.precond = 0;
   const size_t smem = self_smem_doubles(c->p) * sizeof(double);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
@@ -376,6 +377,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
     SA.rec = c->d_rec;
     SA.self = 0;
     SA.alpha = c->d_alpha;
+    SA.precond = 0;
     prof_begin(c, BIE_KIND_SELF, s, &ev);
     k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
     prof_end(c, s, &ev);
@@ -635,6 +637,7 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   SA.rec = c->d_rec;
   SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
   SA.alpha = nullptr;
+  SA.precond = 0;
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
   k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
@@ -871,6 +874,28 @@ struct Krylov {
     k_axpby<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, x, b, y);
     prof_end(c, s, &ev);
   }
+  // y = P^{-1} x, P = 1/2 I + S_self + D_self (block diagonal, exact via the spectra)
+  int prec(const double* x, double* y) {
+    SelfArgs SA;
+    SA.p = c->p;
+    SA.ns = c->ns;
+    SA.mu = c->mu;
+    SA.tab = c->d_tab;
+    SA.centres = c->d_centres;
+    SA.radii = c->d_radii;
+    SA.f = nullptr;
+    SA.q = x;
+    SA.u = y;
+    SA.rec = c->d_rec;
+    SA.self = 1;
+    SA.alpha = nullptr;
+    SA.precond = 1;
+    Ev ev;
+    prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
+    k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
+    prof_end(c, s, &ev);
+    return launch_check(c, "k_self(precond)");
+  }
   // y = (1/2 I + S + D_pv (+ near correction)) x     (BIE 5.4)
   int op(const double* x, double* y) {
     int rc = run_apply(c, x, x, y, BIE_PART_FAR | BIE_PART_SELF, s);
@@ -882,7 +907,8 @@ struct Krylov {
 }  // namespace
 
 int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol, int max_iter,
-                     int restart, int* iters_out, double* resid_out, bie_stream_t st) {
+                     int restart, int precond, int* iters_out, double* resid_out,
+                     bie_stream_t st) {
   if (!c) return BIE_ERR_ARG;
   int rc = check_device(c);
   if (rc) return rc;
@@ -894,16 +920,17 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
     return fail(c, BIE_ERR_ARG, "need tol > 0, max_iter >= 1, 1 <= restart <= 500%s");
   Krylov K{c, (cudaStream_t)st, n};
   const int m = restart;
-  double *V = nullptr, *w = nullptr, *b = nullptr;
+  double *V = nullptr, *w = nullptr, *b = nullptr, *z = nullptr;
   if (cudaMalloc(&V, (size_t)(m + 1) * n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&w, n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&b, n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&z, n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&K.part, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
-    cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(K.part);
+    cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(z); cudaFree(K.part);
     return fail(c, BIE_ERR_ALLOC, "GMRES workspace%s");
   }
-  auto cleanup = [&]() { cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(K.part); };
+  auto cleanup = [&]() { cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(z); cudaFree(K.part); };
   // b = -u_inf, x0 = 0
   cudaMemsetAsync(mu_out, 0, n * sizeof(double), K.s);
   cudaMemsetAsync(b, 0, n * sizeof(double), K.s);
@@ -935,7 +962,12 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
     for (; j < m && it < max_iter; ++j, ++it) {
       double* vj = V + (size_t)j * n;
       double* vn = V + (size_t)(j + 1) * n;
-      if ((rc = K.op(vj, vn))) { cleanup(); return rc; }
+      if (precond) {  // right preconditioning: A P^{-1} v_j
+        if ((rc = K.prec(vj, z)) || (rc = K.op(z, vn))) { cleanup(); return rc; }
+      } else if ((rc = K.op(vj, vn))) {
+        cleanup();
+        return rc;
+      }
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
         const double h = K.dot(vn, V + (size_t)i * n);
         H[(size_t)i * m + j] = h;
@@ -971,7 +1003,14 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
       for (int k = i + 1; k < j; ++k) sacc -= H[(size_t)i * m + k] * y[k];
       y[i] = sacc / H[(size_t)i * m + i];
     }
-    for (int i = 0; i < j; ++i) K.axpby(y[i], V + (size_t)i * n, 1.0, mu_out);
+    if (precond) {  // mu += P^{-1} (V y)
+      cudaMemsetAsync(w, 0, n * sizeof(double), K.s);
+      for (int i = 0; i < j; ++i) K.axpby(y[i], V + (size_t)i * n, 1.0, w);
+      if ((rc = K.prec(w, z))) { cleanup(); return rc; }
+      K.axpby(1.0, z, 1.0, mu_out);
+    } else {
+      for (int i = 0; i < j; ++i) K.axpby(y[i], V + (size_t)i * n, 1.0, mu_out);
+    }
     if (it >= max_iter) done = true;
   }
   // true relative residual of the returned iterate

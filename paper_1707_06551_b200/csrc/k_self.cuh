@@ -37,6 +37,9 @@ struct SelfArgs {
   int self;         // compute the self term (else write zeros)
   double* alpha;    // nullable: [ns][2][nlm][3][2] projections <F,Y e_r>, <F,G>, <F,X>
                     // of (a/mu) f and q, for the near-singular correction (k_near)
+  int precond;      // 1: u = P^{-1} q with P = 1/2 I + S_self + D_self (f ignored):
+                    //    eigenvalue 1/(1/2 + lamS a/mu + lamD) on every VSH mode of
+                    //    degree <= p and 2 on the rest (NEXT-2 preconditioner)
 };
 
 __host__ __device__ inline int64_t self_smem_doubles(int p) {
@@ -198,9 +201,16 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
         aW[d] = ((n + 1) * phG + phY) * i2n;    // eq 2.14
         aX[d] = phX;
       }
-      const double psV = lS[0] * aV[0] + lD[0] * aV[1];
-      const double psW = lS[1] * aW[0] + lD[1] * aW[1];
-      const double psX = lS[2] * aX[0] + lD[2] * aX[1];
+      double psV, psW, psX;
+      if (A.precond) {  // (1/sigma - 2) on the degree-<=p modes; +2 x added in phase E
+        psV = (1.0 / (0.5 + lS[0] * aS + lD[0]) - 2.0) * aV[1];
+        psW = n ? (1.0 / (0.5 + lS[1] * aS + lD[1]) - 2.0) * aW[1] : 0.0;
+        psX = n ? (1.0 / (0.5 + lS[2] * aS + lD[2]) - 2.0) * aX[1] : 0.0;
+      } else {
+        psV = lS[0] * aV[0] + lD[0] * aV[1];
+        psW = lS[1] * aW[0] + lD[1] * aW[1];
+        psX = lS[2] * aX[0] + lD[2] * aX[1];
+      }
       o[0 + ri] = -(n + 1.0) * psV + n * psW;  // psi^Y (eq 2.17)
       o[2 + ri] = psV + psW;                   // psi^G (eq 2.16)
       o[4 + ri] = psX;                         // psi^X
@@ -275,9 +285,17 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
       const double2 t = tw[kk];
       const double cp = t.x, sp = t.y;
       const int64_t i = s * nsn + j * nphi + kk;
-      A.u[3 * i + 0] = v[0] * st * cp + v[1] * ct * cp - v[2] * sp;
-      A.u[3 * i + 1] = v[0] * st * sp + v[1] * ct * sp + v[2] * cp;
-      A.u[3 * i + 2] = v[0] * ct - v[1] * st;
+      double w0 = v[0] * st * cp + v[1] * ct * cp - v[2] * sp;
+      double w1 = v[0] * st * sp + v[1] * ct * sp + v[2] * cp;
+      double w2 = v[0] * ct - v[1] * st;
+      if (A.precond) {
+        w0 = fma(2.0, A.q[3 * i + 0], w0);
+        w1 = fma(2.0, A.q[3 * i + 1], w1);
+        w2 = fma(2.0, A.q[3 * i + 2], w2);
+      }
+      A.u[3 * i + 0] = w0;
+      A.u[3 * i + 1] = w1;
+      A.u[3 * i + 2] = w2;
     }
   }
 }

@@ -29,12 +29,13 @@ def main():
         bie.bie_set_profiling(ctx, True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        it, res = bie.bie_solve_porous(ctx, uinf, mu, tol=1e-10, max_iter=200, restart=50)
+        pc = os.environ.get("PRECOND", "1") == "1"
+        it, res = bie.bie_solve_porous(ctx, uinf, mu, tol=1e-10, max_iter=200, restart=50, precond=pc)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         prof = bie.bie_get_profile(ctx)
         dev_ms = sum(v[0] for v in prof.values())
-        print(json.dumps({"config": cfg, "n_nodes": N, "iterations": it, "rel_resid": res,
+        print(json.dumps({"config": cfg, "precond": pc, "n_nodes": N, "iterations": it, "rel_resid": res,
                           "wall_s": wall, "device_ms": dev_ms,
                           "krylov_ms": prof["krylov"][0], "nbody_ms": prof["nbody"][0],
                           "near_ms": prof["near"][0], "self_ms": prof["self"][0],
