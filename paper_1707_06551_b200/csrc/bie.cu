@@ -279,10 +279,9 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
   SA.alpha = near ? c->d_alpha : nullptr;
   SA.precond = 0;
-  const size_t smem = self_smem_doubles(c->p) * sizeof(double);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
-  k_self<<<(unsigned)c->ns, 128, smem, s>>>(SA);
+  launch_self(SA, s);
   prof_end(c, s, &ev);
   int rc = launch_check(c, "k_self");
   if (rc) return rc;
@@ -379,7 +378,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
     SA.alpha = c->d_alpha;
     SA.precond = 0;
     prof_begin(c, BIE_KIND_SELF, s, &ev);
-    k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
+    launch_self(SA, s);
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_self"))) return rc;
     if ((rc = run_near_coef(c, s))) return rc;
@@ -549,8 +548,7 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
                                                   c->d_x, c->d_n, c->d_w);
   c->launches[BIE_KIND_SETUP] += 2;
   prof_end(c, 0, &ev);
-  const size_t smem = self_smem_doubles(p) * sizeof(double);
-  cudaFuncSetAttribute(k_self, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_self_smem(p);
   cudaFuncSetAttribute(k_near, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p) * sizeof(double)));
   cudaFuncSetAttribute(k_near_off<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -640,7 +638,7 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   SA.precond = 0;
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
-  k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
+  launch_self(SA, s);
   prof_end(c, s, &ev);
   rc = launch_check(c, "k_self");
   if (rc || !(parts & BIE_PART_FAR)) return rc;
@@ -892,7 +890,7 @@ struct Krylov {
     SA.precond = 1;
     Ev ev;
     prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
-    k_self<<<(unsigned)c->ns, 128, self_smem_doubles(c->p) * sizeof(double), s>>>(SA);
+    launch_self(SA, s);
     prof_end(c, s, &ev);
     return launch_check(c, "k_self(precond)");
   }

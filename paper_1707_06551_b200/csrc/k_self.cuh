@@ -50,7 +50,8 @@ __host__ __device__ inline int64_t self_smem_doubles(int p) {
   return C + F + PSI + 2LL * nphi;
 }
 
-__global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
+template <int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
   const TableLayout L(p);
@@ -298,6 +299,19 @@ __global__ void __launch_bounds__(128, 6) k_self(SelfArgs A) {
       A.u[3 * i + 2] = w2;
     }
   }
+}
+
+// Launch configurations chosen by tools/self_tune.cu (profiles/r01_self_tune.txt):
+// small spheres (p <= 8) prefer many 64-thread CTAs, larger ones 128 threads.
+inline void launch_self(const SelfArgs& A, cudaStream_t s) {
+  const size_t smem = self_smem_doubles(A.p) * sizeof(double);
+  if (A.p <= 8) k_self_t<64, 12><<<(unsigned)A.ns, 64, smem, s>>>(A);
+  else k_self_t<128, 4><<<(unsigned)A.ns, 128, smem, s>>>(A);
+}
+inline void set_self_smem(int p) {
+  const int smem = (int)(self_smem_doubles(p) * sizeof(double));
+  cudaFuncSetAttribute(k_self_t<64, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 // Source packing alone (row a2) for the off-surface evaluator; also writes

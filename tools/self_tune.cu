@@ -1,0 +1,78 @@
+// self_tune.cu -- launch-configuration sweep of the self-term kernel k_self_t
+// (timing only; parity is the test suite's job).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/self_tune tools/self_tune.cu
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "../paper_1707_06551_b200/csrc/k_self.cuh"
+
+using namespace bie;
+
+template <int TPB, int MINB>
+void run(const char* name, SelfArgs A, int64_t N) {
+  const size_t smem = self_smem_doubles(A.p) * sizeof(double);
+  cudaFuncSetAttribute(k_self_t<TPB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_self_t<TPB, MINB>, TPB, smem);
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_self_t<TPB, MINB>);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 12; ++r) {
+    cudaEventRecord(e0);
+    k_self_t<TPB, MINB><<<(unsigned)A.ns, TPB, smem>>>(A);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 1 && ms < best) best = ms;
+  }
+  printf("{\"p\": %d, \"variant\": \"%s\", \"regs\": %d, \"spill\": %d, \"occ\": %d, \"us\": %.2f, \"GBps\": %.1f, \"err\": \"%s\"}\n",
+         A.p, name, fa.numRegs, (int)fa.localSizeBytes, occ, best * 1e3, 168.0 * N / (best * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  for (int p : {6, 12}) {
+    const int64_t ns = p == 6 ? 10000 : 4096;
+    const int nsn = (p + 1) * (2 * p + 2);
+    const int64_t N = ns * nsn;
+    const TableLayout L(p);
+    double *tab, *cen, *rad, *f, *q, *u, *rec;
+    cudaMalloc(&tab, L.total * 8);
+    cudaMalloc(&cen, 3 * ns * 8);
+    cudaMalloc(&rad, ns * 8);
+    cudaMalloc(&f, 3 * N * 8);
+    cudaMalloc(&q, 3 * N * 8);
+    cudaMalloc(&u, 3 * N * 8);
+    cudaMalloc(&rec, 12 * N * 8);
+    std::vector<double> h(3 * N);
+    std::mt19937_64 g(1);
+    std::normal_distribution<double> nd;
+    for (auto& v : h) v = nd(g);
+    cudaMemcpy(f, h.data(), 3 * N * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(q, h.data(), 3 * N * 8, cudaMemcpyHostToDevice);
+    std::vector<double> hc(3 * ns), hr(ns, 1.0);
+    for (int64_t s = 0; s < ns; ++s) for (int d = 0; d < 3; ++d) hc[3 * s + d] = 3.0 * s + d;
+    cudaMemcpy(cen, hc.data(), 3 * ns * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(rad, hr.data(), ns * 8, cudaMemcpyHostToDevice);
+    k_gl_rule<<<1, 32>>>(p, tab);
+    k_tables<<<((p + 1) * (p + 1) + 127) / 128, 128>>>(p, tab);
+    SelfArgs A{};
+    A.p = p; A.ns = ns; A.mu = 1.0; A.tab = tab; A.centres = cen; A.radii = rad;
+    A.f = f; A.q = q; A.u = u; A.rec = rec; A.self = 1; A.alpha = nullptr; A.precond = 0;
+    run<128, 6>("T128 minB6 (current)", A, N);
+    run<128, 8>("T128 minB8", A, N);
+    run<128, 4>("T128 minB4", A, N);
+    run<64, 12>("T64 minB12", A, N);
+    run<64, 8>("T64 minB8", A, N);
+    run<256, 3>("T256 minB3", A, N);
+    run<256, 4>("T256 minB4", A, N);
+    run<32, 16>("T32 minB16", A, N);
+    cudaFree(tab); cudaFree(cen); cudaFree(rad); cudaFree(f); cudaFree(q); cudaFree(u); cudaFree(rec);
+  }
+  return 0;
+}
