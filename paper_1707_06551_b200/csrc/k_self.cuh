@@ -121,21 +121,37 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // ---------------------------------------------------------------- B
   // F[dc][j][m] = sum_k g[k] e^{-i m phi_k}
   //   = g0 + (-1)^m g_{p+1} + sum_{k=1}^{p} S_k cos(m phi_k) - i sum_k D_k sin(m phi_k)
-  for (int it = tid; it < 6 * P1 * P1; it += nt) {
-    const int m = it % P1, row = it / P1;
-    const double* g = C + row * nphi;
-    double re = (m & 1) ? g[0] - g[P1] : g[0] + g[P1];
-    double im = 0.0;
-    int idx = m;
-    for (int k = 1; k <= p; ++k) {
-      const double2 t = tw[idx];
-      re = fma(g[k], t.x, re);
-      im = fma(-g[nphi - k], t.y, im);
-      idx += m;
-      if (idx >= nphi) idx -= nphi;
+  // Two azimuthal orders per item (m and m + H, H = ceil(P1/2)) share the row
+  // loads and give two independent accumulation chains.
+  {
+    const int H = (P1 + 1) / 2;
+    for (int it = tid; it < 6 * P1 * H; it += nt) {
+      const int mh = it % H, row = it / H;
+      const int m1 = mh, m2 = mh + H;
+      const bool two = m2 < P1;
+      const double* g = C + row * nphi;
+      double re1 = (m1 & 1) ? g[0] - g[P1] : g[0] + g[P1], im1 = 0.0;
+      double re2 = (m2 & 1) ? g[0] - g[P1] : g[0] + g[P1], im2 = 0.0;
+      int i1 = m1, i2 = two ? m2 : 0;
+      for (int k = 1; k <= p; ++k) {
+        const double gs = g[k], gd = g[nphi - k];
+        const double2 t1 = tw[i1], t2 = tw[i2];
+        re1 = fma(gs, t1.x, re1);
+        im1 = fma(-gd, t1.y, im1);
+        re2 = fma(gs, t2.x, re2);
+        im2 = fma(-gd, t2.y, im2);
+        i1 += m1;
+        if (i1 >= nphi) i1 -= nphi;
+        i2 += m2;
+        if (i2 >= nphi) i2 -= nphi;
+      }
+      F[2 * (row * P1 + m1)] = re1;
+      F[2 * (row * P1 + m1) + 1] = im1;
+      if (two) {
+        F[2 * (row * P1 + m2)] = re2;
+        F[2 * (row * P1 + m2) + 1] = im2;
+      }
     }
-    F[2 * it] = re;
-    F[2 * it + 1] = im;
   }
   __syncthreads();
   // ---------------------------------------------------------------- C
@@ -219,37 +235,42 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   }
   __syncthreads();
   // ---------------------------------------------------------------- D
-  // one (component, latitude, m) per item:
+  // per (latitude, m): U_r from one item, U_theta and U_phi together from
+  // another (they share the dP, mP and psi^G, psi^X loads):
   // U_r = sum_n psiY P, U_t = sum_n psiG dP - i psiX mP, U_p = sum_n i psiG mP + psiX dP
-  for (int it = tid; it < 3 * P1 * P1; it += nt) {
-    const int comp = it / (P1 * P1);
+  for (int it = tid; it < 2 * P1 * P1; it += nt) {
+    const int half = it / (P1 * P1);
     const int j = (it / P1) % P1, m = it % P1;
-    double a0 = 0, a1 = 0;
     const int c0 = lm_index(p, m, m);
     const double* Pj = tab + L.P + (int64_t)j * nlm;
     const double* dPj = tab + L.dP + (int64_t)j * nlm;
     const double* mPj = tab + L.mPs + (int64_t)j * nlm;
-    if (comp == 0) {
+    const int o = j * P1 + m;
+    if (half == 0) {
+      double a0 = 0, a1 = 0;
       for (int c = c0; c < c0 + (P1 - m); ++c) {
+        const double pv = __ldg(Pj + c);
         const double* ps = PSI + 6 * c;
-        a0 = fma(ps[0], Pj[c], a0);
-        a1 = fma(ps[1], Pj[c], a1);
+        a0 = fma(ps[0], pv, a0);
+        a1 = fma(ps[1], pv, a1);
       }
-    } else if (comp == 1) {
-      for (int c = c0; c < c0 + (P1 - m); ++c) {
-        const double* ps = PSI + 6 * c;
-        a0 = fma(ps[2], dPj[c], fma(ps[5], mPj[c], a0));
-        a1 = fma(ps[3], dPj[c], fma(-ps[4], mPj[c], a1));
-      }
+      U[2 * o] = a0;
+      U[2 * o + 1] = a1;
     } else {
+      double t0 = 0, t1 = 0, q0 = 0, q1 = 0;
       for (int c = c0; c < c0 + (P1 - m); ++c) {
+        const double dp = __ldg(dPj + c), mp = __ldg(mPj + c);
         const double* ps = PSI + 6 * c;
-        a0 = fma(ps[4], dPj[c], fma(-ps[3], mPj[c], a0));
-        a1 = fma(ps[5], dPj[c], fma(ps[2], mPj[c], a1));
+        t0 = fma(ps[2], dp, fma(ps[5], mp, t0));
+        t1 = fma(ps[3], dp, fma(-ps[4], mp, t1));
+        q0 = fma(ps[4], dp, fma(-ps[3], mp, q0));
+        q1 = fma(ps[5], dp, fma(ps[2], mp, q1));
       }
+      U[2 * (P1 * P1 + o)] = t0;
+      U[2 * (P1 * P1 + o) + 1] = t1;
+      U[2 * (2 * P1 * P1 + o)] = q0;
+      U[2 * (2 * P1 * P1 + o) + 1] = q1;
     }
-    U[2 * it] = a0;
-    U[2 * it + 1] = a1;
   }
   __syncthreads();
   // ---------------------------------------------------------------- E
