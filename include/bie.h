@@ -208,7 +208,8 @@ int64_t bie_near_pairs(const bie_ctx* ctx);
  * u = u_inf + sum_k (S_k + D_k)[mu] (eq 5.3) and no slip, solve the
  * second-kind BIE (eq 5.4)
  *     (1/2 I + sum_k (S_k + D_k)) [mu] = -u_inf     at every node
- * by restarted GMRES(restart) with modified Gram-Schmidt (the paper names no
+ * by restarted GMRES(restart) with classical Gram-Schmidt applied twice
+ * (batched, one host synchronisation per Arnoldi step; the paper names no
  * solver; SPEC picks GMRES).  The operator is bie_apply_SLDL with f = q = mu
  * (plus the near correction if bie_set_near is on) and the 1/2 I of the
  * exterior limit (reading R14).  Dot products are fixed-order reductions, so

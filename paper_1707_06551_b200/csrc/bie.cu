@@ -518,7 +518,11 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
     return BIE_ERR_CUDA;
   }
   cudaDeviceProp prop;
-  cudaGetDeviceProperties(&prop, c->dev);
+  if (cudaGetDeviceProperties(&prop, c->dev) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return BIE_ERR_CUDA;
+  }
   if (prop.major != 10 || prop.minor != 0) {
     delete c;
     return BIE_ERR_UNSUPPORTED;
@@ -537,8 +541,14 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
     bie_destroy(c);
     return BIE_ERR_ALLOC;
   }
-  cudaMemcpy(c->d_centres, centres_h, 3 * n_spheres * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->d_radii, radii_h, n_spheres * sizeof(double), cudaMemcpyHostToDevice);
+  if (cudaMemcpy(c->d_centres, centres_h, 3 * n_spheres * sizeof(double), cudaMemcpyHostToDevice) !=
+          cudaSuccess ||
+      cudaMemcpy(c->d_radii, radii_h, n_spheres * sizeof(double), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    bie_destroy(c);
+    return BIE_ERR_CUDA;
+  }
   // row a1: GL rule -> tables -> nodes (default stream, synchronous)
   Ev ev;
   prof_begin(c, BIE_KIND_SETUP, 0, &ev);
@@ -703,14 +713,17 @@ int bie_apply_SLDL_host(bie_ctx* c, const double* f_h, const double* q_h, double
   cudaStream_t st = (cudaStream_t)s;
   Ev ev;
   prof_begin(c, BIE_KIND_COPY, st, &ev);
-  cudaMemcpyAsync(c->d_f, f_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->d_q, q_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaError_t ce = cudaMemcpyAsync(c->d_f, f_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(c->d_q, q_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
   prof_end(c, st, &ev);
+  if (ce != cudaSuccess) return cuda_fail(c, ce, "bie_apply_SLDL_host: H2D");
   rc = run_apply(c, c->d_f, c->d_q, c->d_u, BIE_PART_FAR | BIE_PART_SELF, st);
   if (rc) return rc;
   prof_begin(c, BIE_KIND_COPY, st, &ev);
-  cudaMemcpyAsync(u_h, c->d_u, n3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  ce = cudaMemcpyAsync(u_h, c->d_u, n3 * sizeof(double), cudaMemcpyDeviceToHost, st);
   prof_end(c, st, &ev);
+  if (ce != cudaSuccess) return cuda_fail(c, ce, "bie_apply_SLDL_host: D2H");
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(c, e, "bie_apply_SLDL_host");
   return BIE_OK;
@@ -740,17 +753,23 @@ int bie_eval_offsurface_host(bie_ctx* c, const double* f_h, const double* q_h, c
   cudaStream_t st = (cudaStream_t)s;
   Ev ev;
   prof_begin(c, BIE_KIND_COPY, st, &ev);
-  if (f_h) cudaMemcpyAsync(c->d_f, f_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
-  if (q_h) cudaMemcpyAsync(c->d_q, q_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->d_tg, tg_h, 3 * m * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaError_t ce = cudaSuccess;
+  if (f_h) ce = cudaMemcpyAsync(c->d_f, f_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (q_h && ce == cudaSuccess)
+    ce = cudaMemcpyAsync(c->d_q, q_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(c->d_tg, tg_h, 3 * m * sizeof(double), cudaMemcpyHostToDevice, st);
   prof_end(c, st, &ev);
+  if (ce != cudaSuccess) return cuda_fail(c, ce, "bie_eval_offsurface_host: H2D");
   rc = run_offsurface(c, f_h ? c->d_f : nullptr, q_h ? c->d_q : nullptr, c->d_tg, m, c->d_uo,
                       p_h ? c->d_po : nullptr, st);
   if (rc) return rc;
   prof_begin(c, BIE_KIND_COPY, st, &ev);
-  cudaMemcpyAsync(u_h, c->d_uo, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, st);
-  if (p_h) cudaMemcpyAsync(p_h, c->d_po, m * sizeof(double), cudaMemcpyDeviceToHost, st);
+  ce = cudaMemcpyAsync(u_h, c->d_uo, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (p_h && ce == cudaSuccess)
+    ce = cudaMemcpyAsync(p_h, c->d_po, m * sizeof(double), cudaMemcpyDeviceToHost, st);
   prof_end(c, st, &ev);
+  if (ce != cudaSuccess) return cuda_fail(c, ce, "bie_eval_offsurface_host: D2H");
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(c, e, "bie_eval_offsurface_host");
   return BIE_OK;
@@ -815,7 +834,12 @@ int bie_set_near(bie_ctx* c, double eta) {
   const unsigned g = (unsigned)((ns + 127) / 128);
   k_near_lists<<<g, 128>>>(ns, c->d_centres, c->d_radii, eta, d_cnt, nullptr, nullptr);
   std::vector<int> cnt(ns), off(ns + 1, 0), tgt;
-  cudaMemcpy(cnt.data(), d_cnt, ns * sizeof(int), cudaMemcpyDeviceToHost);
+  if (cudaMemcpy(cnt.data(), d_cnt, ns * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaError_t e = cudaGetLastError();
+    cudaFree(d_cnt);
+    near_free(c);
+    return cuda_fail(c, e, "bie_set_near: neighbour counts");
+  }
   for (int64_t t = 0; t < ns; ++t) {
     off[t + 1] = off[t] + cnt[t];
     if (cnt[t]) tgt.push_back((int)t);
@@ -837,8 +861,14 @@ int bie_set_near(bie_ctx* c, double eta) {
     near_free(c);
     return fail(c, BIE_ERR_ALLOC, "near lists%s");
   }
-  cudaMemcpy(c->d_nb_off, off.data(), (ns + 1) * sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->d_near_tgt, tgt.data(), tgt.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (cudaMemcpy(c->d_nb_off, off.data(), (ns + 1) * sizeof(int), cudaMemcpyHostToDevice) !=
+          cudaSuccess ||
+      cudaMemcpy(c->d_near_tgt, tgt.data(), tgt.size() * sizeof(int), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaError_t e = cudaGetLastError();
+    near_free(c);
+    return cuda_fail(c, e, "bie_set_near: lists");
+  }
   k_near_lists<<<g, 128>>>(ns, c->d_centres, c->d_radii, eta, nullptr, c->d_nb_off, c->d_nb_idx);
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -866,6 +896,26 @@ struct Krylov {
     cudaStreamSynchronize(s);
     return h;
   }
+  // classical Gram-Schmidt twice against V[0..nv): on return hv[0..nv) holds
+  // the projections (device), w is orthogonalised, and wnorm2 = w.w; one sync.
+  void cgs2(const double* V, int nv, double* w, double* dh, double* hv, double* wnorm2) {
+    Ev ev;
+    prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
+    for (int pass = 0; pass < 2; ++pass) {
+      k_mdot_partial<<<kDotBlocks, kDotThreads, 0, s>>>(n, nv, V, w, mpart);
+      k_mdot_final<<<nv, kDotThreads, 0, s>>>(mpart, dh + pass * 512, 0);
+      k_maxpy<<<kDotBlocks, kDotThreads, 0, s>>>(n, nv, dh + pass * 512, V, w);
+    }
+    k_dot_partial<<<kDotBlocks, kDotThreads, 0, s>>>(n, w, w, part);
+    k_dot_final<<<1, kDotThreads, 0, s>>>(part, dh + 1024);
+    prof_end(c, s, &ev);
+    std::vector<double> hh(1025);
+    cudaMemcpyAsync(hh.data(), dh, 1025 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    for (int i = 0; i < nv; ++i) hv[i] = hh[i] + hh[512 + i];
+    *wnorm2 = hh[1024];
+  }
+  double* mpart = nullptr;  // [512][kDotBlocks]
   void axpby(double a, const double* x, double b, double* y) {
     Ev ev;
     prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
@@ -916,19 +966,26 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
   if (overlaps(uinf, n, mu_out, n)) return fail(c, BIE_ERR_ARG, "mu overlaps uinf%s");
   if (!(tol > 0.0) || max_iter < 1 || restart < 1 || restart > 500)
     return fail(c, BIE_ERR_ARG, "need tol > 0, max_iter >= 1, 1 <= restart <= 500%s");
+  // (restart + 1 <= 512 Krylov vectors: fits the batched Gram-Schmidt buffers)
   Krylov K{c, (cudaStream_t)st, n};
   const int m = restart;
-  double *V = nullptr, *w = nullptr, *b = nullptr, *z = nullptr;
+  double *V = nullptr, *w = nullptr, *b = nullptr, *z = nullptr, *dh = nullptr;
   if (cudaMalloc(&V, (size_t)(m + 1) * n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&w, n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&b, n * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&z, n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&dh, 1025 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&K.mpart, (size_t)512 * kDotBlocks * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&K.part, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
-    cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(z); cudaFree(K.part);
+    cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(z); cudaFree(dh); cudaFree(K.mpart);
+    cudaFree(K.part);
     return fail(c, BIE_ERR_ALLOC, "GMRES workspace%s");
   }
-  auto cleanup = [&]() { cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(z); cudaFree(K.part); };
+  auto cleanup = [&]() {
+    cudaFree(V); cudaFree(w); cudaFree(b); cudaFree(z); cudaFree(dh); cudaFree(K.mpart);
+    cudaFree(K.part);
+  };
   // b = -u_inf, x0 = 0
   cudaMemsetAsync(mu_out, 0, n * sizeof(double), K.s);
   cudaMemsetAsync(b, 0, n * sizeof(double), K.s);
@@ -966,12 +1023,12 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
         cleanup();
         return rc;
       }
-      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
-        const double h = K.dot(vn, V + (size_t)i * n);
-        H[(size_t)i * m + j] = h;
-        K.axpby(-h, V + (size_t)i * n, 1.0, vn);
-      }
-      const double hn = std::sqrt(K.dot(vn, vn));
+      // classical Gram-Schmidt applied twice (CGS2): batched, one host sync
+      std::vector<double> hcol(j + 1);
+      double wn2 = 0.0;
+      K.cgs2(V, j + 1, vn, dh, hcol.data(), &wn2);
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i];
+      const double hn = std::sqrt(wn2);
       H[(size_t)(j + 1) * m + j] = hn;
       if (hn > 0.0) K.axpby(0.0, vn, 1.0 / hn, vn);
       for (int i = 0; i < j; ++i) {  // apply previous Givens rotations

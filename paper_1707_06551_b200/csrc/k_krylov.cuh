@@ -52,3 +52,46 @@ __global__ void __launch_bounds__(kDotThreads) k_dot_final(const double* __restr
 }
 
 }  // namespace bie
+
+namespace bie {
+
+// part[i][b] = block b's partial of  V_i . w,  i < nv   (fixed grid)
+__global__ void __launch_bounds__(kDotThreads) k_mdot_partial(int64_t n, int nv,
+                                                              const double* __restrict__ V,
+                                                              const double* __restrict__ w,
+                                                              double* __restrict__ part) {
+  __shared__ double red[kDotThreads / 32];
+  for (int i = 0; i < nv; ++i) {
+    const double* v = V + (int64_t)i * n;
+    double s = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)kDotThreads + threadIdx.x; e < n;
+         e += (int64_t)kDotBlocks * kDotThreads)
+      s = fma(v[e], w[e], s);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) part[(int64_t)i * kDotBlocks + blockIdx.x] = s;
+    __syncthreads();
+  }
+}
+
+// out[i] (+)= sum_b part[i][b]   (one block per vector; accumulate: out[i] += ...)
+__global__ void __launch_bounds__(kDotThreads) k_mdot_final(const double* __restrict__ part,
+                                                            double* __restrict__ out, int accumulate) {
+  __shared__ double red[kDotThreads / 32];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < kDotBlocks; b += kDotThreads) s += part[(int64_t)blockIdx.x * kDotBlocks + b];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = accumulate ? out[blockIdx.x] + s : s;
+}
+
+// w -= sum_i h_i V_i   (h on the device; fixed order in i)
+__global__ void k_maxpy(int64_t n, int nv, const double* __restrict__ h,
+                        const double* __restrict__ V, double* __restrict__ w) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = w[e];
+    for (int i = 0; i < nv; ++i) s = fma(-h[i], V[(int64_t)i * n + e], s);
+    w[e] = s;
+  }
+}
+
+}  // namespace bie
