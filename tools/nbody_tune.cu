@@ -103,18 +103,12 @@ int main(int argc, char** argv) {
   const double pairs_apply = (double)N * (N - nsn), pairs_off = (double)N * N;
   const int sm = prop.multiProcessorCount;
   printf("# N = %lld, SMs = %d\n", (long long)N, sm);
-  run<4, 128, 64, 3, false, 1, 2>("apply R4 T128 TS64 (current)", A, sm, pairs_apply, reps);
-  run<8, 64, 64, 3, false, 1, 1>("apply R8 T64 u1", A, sm, pairs_apply, reps);
-  run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 u2", A, sm, pairs_apply, reps);
-  run<8, 128, 64, 3, false, 1, 1>("apply R8 T128 u1", A, sm, pairs_apply, reps);
-  run<8, 32, 64, 3, false, 1, 1>("apply R8 T32 u1", A, sm, pairs_apply, reps);
-  run<8, 64, 128, 3, false, 1, 1>("apply R8 T64 TS128 u1", A, sm, pairs_apply, reps);
-  run<10, 64, 64, 3, false, 1, 1>("apply R10 T64 u1", A, sm, pairs_apply, reps);
-  run<12, 32, 64, 3, false, 1, 1>("apply R12 T32 u1", A, sm, pairs_apply, reps);
-  run<6, 64, 64, 3, false, 1, 1>("apply R6 T64 u1", A, sm, pairs_apply, reps);
-  run<6, 64, 64, 3, false, 1, 2>("apply R6 T64 u2", A, sm, pairs_apply, reps);
-  run<4, 128, 64, 3, true, 1, 2>("off R4 T128 (current)", A, sm, pairs_off, reps);
-  run<8, 64, 64, 3, true, 1, 1>("off R8 T64 u1", A, sm, pairs_off, reps);
-  run<6, 64, 64, 3, true, 1, 1>("off R6 T64 u1", A, sm, pairs_off, reps);
+  run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 u2 (library)", A, sm, pairs_apply, reps);
+  run<8, 64, 64, 3, true, 1, 1>("off R8 T64 u1 (library)", A, sm, pairs_off, reps);
+  run<8, 64, 64, 3, true, 1, 2>("off R8 T64 u2", A, sm, pairs_off, reps);
+  run<8, 64, 128, 3, true, 1, 1>("off R8 T64 TS128 u1", A, sm, pairs_off, reps);
+  run<8, 32, 64, 3, true, 1, 1>("off R8 T32 u1", A, sm, pairs_off, reps);
+  run<7, 64, 64, 3, true, 1, 1>("off R7 T64 u1", A, sm, pairs_off, reps);
+  run<6, 64, 64, 3, true, 1, 2>("off R6 T64 u2", A, sm, pairs_off, reps);
   return 0;
 }
