@@ -42,7 +42,7 @@ typedef void* bie_stream_t; /* cudaStream_t */
 enum bie_status {
   BIE_OK = 0,
   BIE_ERR_ARG = 1,         /* bad pointer, size, value or aliasing          */
-  BIE_ERR_GEOMETRY = 2,    /* overlapping spheres (|c_i-c_j| < a_i + a_j)   */
+  BIE_ERR_GEOMETRY = 2,    /* overlapping/touching spheres (|c_i-c_j| <= a_i + a_j) */
   BIE_ERR_ALLOC = 3,       /* device allocation failed                      */
   BIE_ERR_CUDA = 4,        /* CUDA launch/runtime error                     */
   BIE_ERR_UNSUPPORTED = 5  /* p outside [1, BIE_P_MAX] or no sm_100a device  */
@@ -76,7 +76,9 @@ enum bie_status {
  *   Weights w = a^2 lambda_j 2 pi/(2p+2) (eq 4.4, reading R4);
  *   outward normals.  Synchronous.  Returns BIE_ERR_ARG on NULL or
  *   non-finite input, n_spheres < 1 or radii <= 0; BIE_ERR_GEOMETRY if two
- *   spheres overlap (SPEC "no two spheres overlap", R19); BIE_ERR_UNSUPPORTED
+ *   spheres overlap or touch (|c_i - c_j| <= a_i + a_j; SPEC's "pairwise
+ *   center distance > sum of radii", R19 -- touching spheres can place a node
+ *   of each at the contact point, r = 0); BIE_ERR_UNSUPPORTED
  *   for p out of range.  *out is NULL on failure.
  */
 int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres, int p,

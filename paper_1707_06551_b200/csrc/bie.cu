@@ -145,7 +145,7 @@ static int check_device(bie_ctx* c) {
   return BIE_OK;
 }
 
-// Overlap test with a uniform cell list (cell = 2 max radius): O(n_spheres).
+// Overlap/contact test with a uniform cell list (cell = 2 max radius): O(n_spheres).
 static bool spheres_overlap(const double* c, const double* a, int64_t n, int64_t* bad_i, int64_t* bad_j) {
   double amax = 0;
   for (int64_t i = 0; i < n; ++i) amax = std::max(amax, a[i]);
@@ -171,7 +171,7 @@ static bool spheres_overlap(const double* c, const double* a, int64_t n, int64_t
             double r2 = 0;
             for (int d = 0; d < 3; ++d) r2 += (c[3 * i + d] - c[3 * j + d]) * (c[3 * i + d] - c[3 * j + d]);
             double lim = a[i] + a[j];
-            if (r2 < lim * lim) {
+            if (r2 <= lim * lim) {  // touching spheres can share a node (r = 0)
               *bad_i = i;
               *bad_j = j;
               return true;

@@ -53,8 +53,10 @@ def test_create_validation(abi):
     assert _mk(c, [1.0, -1.0], 2, 4, 1.0, abi)[0] == abi.BIE_ERR_ARG
     assert _mk([[0, 0, np.inf], [3, 0, 0]], a, 2, 4, 1.0, abi)[0] == abi.BIE_ERR_ARG
     assert _mk([[0, 0, 0], [1.9, 0, 0]], a, 2, 4, 1.0, abi)[0] == abi.BIE_ERR_GEOMETRY
-    # touching is allowed (|c_i - c_j| == a_i + a_j is not an overlap)
-    rc, h = _mk([[0, 0, 0], [2.0, 0, 0]], a, 2, 4, 1.0, abi)
+    # touching is rejected too (SPEC: centre distance > sum of radii): at even p
+    # both spheres would carry a node at the contact point
+    assert _mk([[0, 0, 0], [2.0, 0, 0]], a, 2, 4, 1.0, abi)[0] == abi.BIE_ERR_GEOMETRY
+    rc, h = _mk([[0, 0, 0], [2.0 + 1e-9, 0, 0]], a, 2, 4, 1.0, abi)
     assert rc != abi.BIE_ERR_GEOMETRY
 
 

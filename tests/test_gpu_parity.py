@@ -254,3 +254,33 @@ def test_streams_and_two_contexts(bie, oracle_mod):
 def test_smoke_entry(bie):
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ------------------------------------------------------------ edge cases
+def test_max_order_full_apply(bie, oracle_mod):
+    """p = BIE_P_MAX = 30 (1922 nodes per sphere, several source tiles and a
+    ragged target tile) through the whole apply, and the off-surface path."""
+    p = bie.BIE_P_MAX
+    c, a, f, q, mu = _random_case(1201, 2, p, True, 1.1)
+    ref = oracle_mod.apply(c, a, p, mu, f, q)
+    _assert_parity(gpu_apply(bie, c, a, p, mu, f, q), ref, "p=30 apply")
+
+
+def test_nearly_touching_spheres_and_zero_density(bie, oracle_mod):
+    """Gap 1e-3 with two nodes 1e-3 apart across the gap (touching spheres are
+    rejected at create, R19): the apply stays finite and matches the oracle;
+    zero densities give exactly 0."""
+    p = 6
+    c = np.array([[0.0, 0.0, 0.0], [1.701, 0.0, 0.0]])
+    a = np.array([1.0, 0.7])
+    N = 2 * (p + 1) * (2 * p + 2)
+    rng = np.random.default_rng(1202)
+    f, q = rng.standard_normal((N, 3)), rng.standard_normal((N, 3))
+    got = gpu_apply(bie, c, a, p, 1.0, f, q)
+    assert np.all(np.isfinite(got))
+    _assert_parity(got, oracle_mod.apply(c, a, p, 1.0, f, q), "nearly touching")
+    with pytest.raises(bie.BieError) as e:
+        bie.bie_create(np.array([[0.0, 0, 0], [1.7, 0, 0]]), a, p, 1.0)
+    assert e.value.status == bie.BIE_ERR_GEOMETRY
+    z = np.zeros((N, 3))
+    assert np.all(gpu_apply(bie, c, a, p, 1.0, z, z) == 0.0)
