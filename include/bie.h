@@ -193,9 +193,10 @@ int bie_reset_profile(bie_ctx* ctx);
  * expansion (eqs 3.6-3.11 with reading R1, eq 4.7; the expansion is the
  * discrete projection of reading R9).  eta = 0 disables it (the default, and
  * the BASELINE.json metric path).  bie_eval_offsurface applies the same
- * correction to u and p at every target x within eta * 2 a_s of the surface
- * of a sphere s (|x - c_s| - a_s < eta * 2 a_s, SPEC's point-to-surface form
- * of eq 4.5), using the exterior pressures of P:189 (S) and reading R12 (D).
+ * correction to u and p at every EXTERIOR target x within eta * 2 a_s of the
+ * surface of a sphere s (0 <= |x - c_s| - a_s < eta * 2 a_s, SPEC's
+ * point-to-surface form of eq 4.5), using the exterior pressures of P:189 (S)
+ * and reading R12 (D); targets inside a sphere keep the plain smooth sum.
  * Builds the neighbour lists on the device and synchronises.  BIE_ERR_ARG for
  * eta < 0 or non-finite.
  */

@@ -794,7 +794,8 @@ extern "C" int oracle_near_offsurface(const double* centres, const double* radii
   const int nsn = G.nsn;
   auto near_pt = [&](int64_t s, const double* x) {
     const double dx = x[0] - centres[3 * s], dy = x[1] - centres[3 * s + 1], dz = x[2] - centres[3 * s + 2];
-    return std::sqrt(dx * dx + dy * dy + dz * dz) - radii[s] < eta * 2.0 * radii[s];
+    const double d = std::sqrt(dx * dx + dy * dy + dz * dz) - radii[s];
+    return d >= 0.0 && d < eta * 2.0 * radii[s];  // exterior targets only (eqs 3.6-3.11 r >= 1)
   };
   std::vector<char> need(ns, 0);
   for (int64_t t = 0; t < m; ++t)

@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
                    dz = __dsub_rn(x[2], tile[4 * e + 2]);
       const double a = tile[4 * e + 3];
       const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-      if (live && __dsub_rn(r, a) < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {
+      const double dsurf = __dsub_rn(r, a);
+      if (live && dsurf >= 0.0 && dsurf < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {  // exterior only
         list[cnt++] = (int)(s0 + e);
         if (cnt == kNearList) flush();
       }

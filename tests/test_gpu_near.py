@@ -136,6 +136,7 @@ def _near_targets(c, a, n, seed, lo=0.1, hi=1.5):
 def test_offsurface_near_matches_oracle(bie, oracle_mod, p, ns, eta, use_p):
     c, a, f, q, mu = _random_case(900 + p, ns, p, True, 1.4)
     tg = _near_targets(c, a, 300, p)
+    tg = np.concatenate([tg, c[:2] + np.array([[0.1, -0.2, 0.15]])])  # two interior targets
     uref, pref = oracle_mod.offsurface_near(c, a, p, mu, f, q, eta, tg)
     ctx = bie.bie_create(c, a, p, mu)
     bie.bie_set_near(ctx, eta)
