@@ -466,3 +466,32 @@ def test_committed_golden_fixture(oracle_mod):
     d = make_config(1)
     u = oracle_mod.apply(d["centres"], d["radii"], 4, 1.0, d["f"], d["q"])
     assert np.max(np.abs(u - np.array(gold["u"]))) <= 1e-15 * 4
+
+
+# ------------------------------------- structure of the self operator (R9)
+@pytest.mark.parametrize("p", [3, 5])
+def test_self_operator_structure_on_white_noise(oracle_mod, p):
+    """For non-band-limited input the paper pins nothing (R9); what the discrete
+    projection must still satisfy: the self operator sum_nZ lam Pi_nZ is
+    self-adjoint in the quadrature inner product <a,b>_w = sum w a.b (the
+    projectors are w-orthogonal), for S and for D_pv separately, and its rank is
+    3(p+1)^2 - 2 (W_0 = X_0 = 0; every other mode has a non-zero eigenvalue,
+    except V_0 for S whose eigenvalue is 0)."""
+    ns = (p + 1) * (2 * p + 2)
+    c, a = np.zeros((1, 3)), np.ones(1)
+    _, _, w = oracle_mod.nodes(c, a, p)
+    MS = np.empty((3 * ns, 3 * ns))
+    MD = np.empty((3 * ns, 3 * ns))
+    for col in range(3 * ns):
+        e = np.zeros((ns, 3))
+        e.reshape(-1)[col] = 1.0
+        MS[:, col] = oracle_mod.self_term(c, a, p, 1.0, e, None).reshape(-1)
+        MD[:, col] = oracle_mod.self_term(c, a, p, 1.0, None, e).reshape(-1)
+    W = np.repeat(w, 3)
+    for M in (MS, MD):
+        A = W[:, None] * M                          # <e_i, M e_j>_w
+        assert np.abs(A - A.T).max() <= 1e-14 * np.abs(A).max()
+    sv = np.linalg.svd(MD, compute_uv=False)
+    assert np.sum(sv > 1e-10 * sv[0]) == 3 * (p + 1) ** 2 - 2
+    sv = np.linalg.svd(MS, compute_uv=False)
+    assert np.sum(sv > 1e-10 * sv[0]) == 3 * (p + 1) ** 2 - 3   # lamS_V(0) = 0
