@@ -306,7 +306,10 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   NA.nb_idx = c->d_nb_idx;
   NA.u = u;
   prof_begin(c, BIE_KIND_NEAR, s, &ev);
-  k_near<<<(unsigned)c->n_near_tgt, 128, near_smem_doubles(c->p) * sizeof(double), s>>>(NA);
+  const bool stage = near_stage(c->p);
+  const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
+  if (stage) k_near<true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+  else k_near<false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
   prof_end(c, s, &ev);
   return launch_check(c, "k_near");
 }
@@ -559,8 +562,10 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   c->launches[BIE_KIND_SETUP] += 2;
   prof_end(c, 0, &ev);
   set_self_smem(p);
-  cudaFuncSetAttribute(k_near, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_smem_doubles(p) * sizeof(double)));
+  cudaFuncSetAttribute(k_near<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_smem_doubles(p, true) * sizeof(double)));
+  cudaFuncSetAttribute(k_near<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_smem_doubles(p, false) * sizeof(double)));
   cudaFuncSetAttribute(k_near_off<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_off_smem_doubles(p) * sizeof(double)));
   cudaFuncSetAttribute(k_near_off<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -59,10 +59,13 @@ struct NearArgs {
   double* u;             // [N][3], accumulated
 };
 
-__host__ __device__ inline int64_t near_smem_doubles(int p) {
+__host__ __device__ inline int64_t near_smem_doubles(int p, bool stage) {
   const int nlm = (p + 1) * (p + 2) / 2, nsn = (p + 1) * (2 * p + 2);
-  return 3LL * nsn + 3LL * nlm;
+  return 3LL * nsn + ((3LL * nlm + 1) & ~1LL) + (stage ? 12LL * nsn + 10LL * nlm : 0);
 }
+
+// stage the source sphere's records and coefficients in shared memory when they fit
+__host__ __device__ inline bool near_stage(int p) { return near_smem_doubles(p, true) * 8 <= 160 * 1024; }
 
 template <bool PRESSURE>
 __device__ __forceinline__ void exterior_field(int p, const double* __restrict__ cf,
@@ -72,6 +75,9 @@ __device__ __forceinline__ void exterior_field(int p, const double* __restrict__
 
 // One CTA per target sphere t with near neighbours; for each neighbour s (in
 // ascending index) every thread adds exterior_s(x) - smooth_s(x) at its nodes.
+// STAGE: s's packed records and expansion coefficients are copied to shared
+// memory first (broadcast reads in the O(n_s^2) smooth-rule subtraction).
+template <bool STAGE>
 __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, nsn = A.nsn;
@@ -79,17 +85,33 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   const int nlm = L.nlm;
   double* du = sm;              // [nsn][3]
   double* rt = du + 3 * nsn;    // rA, rB, rC [3][nlm]
+  double* srec = rt + ((3 * nlm + 1) & ~1);  // STAGE: [nsn][12] (16-byte aligned)
+  double* scf = srec + 12 * nsn;  // STAGE: [nlm][10]
   const int tid = threadIdx.x, nt = blockDim.x;
   const int t = A.tgt[blockIdx.x];
   for (int e = tid; e < 3 * nlm; e += nt) rt[e] = A.tab[L.rA + e];
   for (int e = tid; e < 3 * nsn; e += nt) du[e] = 0.0;
-  __syncthreads();
   for (int qn = A.nb_off[t]; qn < A.nb_off[t + 1]; ++qn) {
     const int s = A.nb_idx[qn];
     const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
     const double a = A.radii[s];
     const double* cf = A.coef + (int64_t)s * nlm * 10;
-    const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
+    const double* rec_s = A.rec + (int64_t)s * nsn * kRec;
+    if (STAGE) {
+      __syncthreads();  // previous neighbour's staged data no longer in use
+      const double2* g2 = reinterpret_cast<const double2*>(rec_s);
+      double2* s2 = reinterpret_cast<double2*>(srec);
+      for (int e = tid; e < 6 * nsn; e += nt) s2[e] = g2[e];
+      const double2* c2 = reinterpret_cast<const double2*>(cf);
+      double2* d2 = reinterpret_cast<double2*>(scf);
+      for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
+      __syncthreads();
+      cf = scf;
+      rec_s = srec;
+    } else if (qn == A.nb_off[t]) {
+      __syncthreads();
+    }
+    const double2* sr = reinterpret_cast<const double2*>(rec_s);
     for (int kk = tid; kk < nsn; kk += nt) {
       const int64_t i = (int64_t)t * nsn + kk;
       const double xt[3] = {A.rec[i * kRec], A.rec[i * kRec + 1], A.rec[i * kRec + 2]};
@@ -98,8 +120,7 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
       double acc[3] = {0.0, 0.0, 0.0}, pdummy = 0.0;
       for (int k = 0; k < nsn; ++k) {
         const double2* q2 = sr + k * (kRec / 2);
-        pair_acc<false, false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3), __ldg(q2 + 4),
-                               __ldg(q2 + 5), 0.0, xt, acc, pdummy, 0, 0, 1);
+        pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
       }
       du[3 * kk + 0] += ex[0] - acc[0];
       du[3 * kk + 1] += ex[1] - acc[1];
