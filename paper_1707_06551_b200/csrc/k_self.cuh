@@ -50,10 +50,12 @@ __host__ __device__ inline int64_t self_smem_doubles(int p) {
   return C + F + PSI + 2LL * nphi;
 }
 
-template <int TPB, int MINB>
+// PT > 0: the order p is the compile-time constant PT (loop bounds, index
+// decoding and strides fold away); PT = 0: generic runtime p.
+template <int TPB, int MINB, int PT = 0>
 __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   extern __shared__ __align__(16) double sm[];
-  const int p = A.p, P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
+  const int p = PT > 0 ? PT : A.p, P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
   const TableLayout L(p);
   const int nlm = L.nlm;
   double* C = sm;                          // [2][3][nsn]
@@ -324,15 +326,29 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
 
 // Launch configurations chosen by tools/self_tune.cu (profiles/r01_self_tune.txt):
 // small spheres (p <= 8) prefer many 64-thread CTAs, larger ones 128 threads.
+// The orders of the BASELINE configurations (4, 6, 8, 12) get compile-time-p
+// instantiations; every other p runs the generic kernel.
 inline void launch_self(const SelfArgs& A, cudaStream_t s) {
   const size_t smem = self_smem_doubles(A.p) * sizeof(double);
-  if (A.p <= 8) k_self_t<64, 12><<<(unsigned)A.ns, 64, smem, s>>>(A);
-  else k_self_t<128, 4><<<(unsigned)A.ns, 128, smem, s>>>(A);
+  const unsigned g = (unsigned)A.ns;
+  switch (A.p) {
+    case 4: k_self_t<64, 12, 4><<<g, 64, smem, s>>>(A); break;
+    case 6: k_self_t<64, 12, 6><<<g, 64, smem, s>>>(A); break;
+    case 8: k_self_t<64, 12, 8><<<g, 64, smem, s>>>(A); break;
+    case 12: k_self_t<128, 4, 12><<<g, 128, smem, s>>>(A); break;
+    default:
+      if (A.p <= 8) k_self_t<64, 12><<<g, 64, smem, s>>>(A);
+      else k_self_t<128, 4><<<g, 128, smem, s>>>(A);
+  }
 }
 inline void set_self_smem(int p) {
   const int smem = (int)(self_smem_doubles(p) * sizeof(double));
   cudaFuncSetAttribute(k_self_t<64, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_self_t<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 12, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 12, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<128, 4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 // Source packing alone (row a2) for the off-surface evaluator; also writes

@@ -9,21 +9,21 @@
 
 using namespace bie;
 
-template <int TPB, int MINB>
+template <int TPB, int MINB, int PT = 0>
 void run(const char* name, SelfArgs A, int64_t N) {
   const size_t smem = self_smem_doubles(A.p) * sizeof(double);
-  cudaFuncSetAttribute(k_self_t<TPB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_self_t<TPB, MINB, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_self_t<TPB, MINB>, TPB, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_self_t<TPB, MINB, PT>, TPB, smem);
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, k_self_t<TPB, MINB>);
+  cudaFuncGetAttributes(&fa, k_self_t<TPB, MINB, PT>);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
   for (int r = 0; r < 12; ++r) {
     cudaEventRecord(e0);
-    k_self_t<TPB, MINB><<<(unsigned)A.ns, TPB, smem>>>(A);
+    k_self_t<TPB, MINB, PT><<<(unsigned)A.ns, TPB, smem>>>(A);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -64,14 +64,19 @@ int main() {
     SelfArgs A{};
     A.p = p; A.ns = ns; A.mu = 1.0; A.tab = tab; A.centres = cen; A.radii = rad;
     A.f = f; A.q = q; A.u = u; A.rec = rec; A.self = 1; A.alpha = nullptr; A.precond = 0;
-    run<128, 6>("T128 minB6 (current)", A, N);
-    run<128, 8>("T128 minB8", A, N);
-    run<128, 4>("T128 minB4", A, N);
-    run<64, 12>("T64 minB12", A, N);
-    run<64, 8>("T64 minB8", A, N);
-    run<256, 3>("T256 minB3", A, N);
-    run<256, 4>("T256 minB4", A, N);
-    run<32, 16>("T32 minB16", A, N);
+    run<64, 12>("T64 minB12 generic", A, N);
+    run<128, 4>("T128 minB4 generic", A, N);
+    if (p == 6) {
+      run<64, 12, 6>("T64 minB12 PT=6", A, N);
+      run<128, 6, 6>("T128 minB6 PT=6", A, N);
+      run<64, 8, 6>("T64 minB8 PT=6", A, N);
+      run<32, 16, 6>("T32 minB16 PT=6", A, N);
+    } else {
+      run<128, 4, 12>("T128 minB4 PT=12", A, N);
+      run<128, 6, 12>("T128 minB6 PT=12", A, N);
+      run<256, 3, 12>("T256 minB3 PT=12", A, N);
+      run<64, 8, 12>("T64 minB8 PT=12", A, N);
+    }
     cudaFree(tab); cudaFree(cen); cudaFree(rad); cudaFree(f); cudaFree(q); cudaFree(u); cudaFree(rec);
   }
   return 0;
