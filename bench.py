@@ -144,6 +144,8 @@ class ClockSampler:
 # ------------------------------------------------------------------ GPU arm
 def run_gpu(args):
     import torch
+    import __graft_entry__
+    __graft_entry__.build()  # no-op when libbie.so is up to date
     import paper_1707_06551_b200 as bie
     rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)

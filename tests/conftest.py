@@ -13,6 +13,13 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
+@pytest.fixture(scope="session", autouse=True)
+def _built_native():
+    """(Re)build libbie.so and the oracle if missing or stale (no-op otherwise)."""
+    import __graft_entry__
+    __graft_entry__.build()
+
+
 @pytest.fixture(scope="session")
 def oracle_mod():
     import oracle
