@@ -29,10 +29,11 @@ _DP = ctypes.POINTER(ctypes.c_double)
 def build_oracle(force: bool = False) -> str:
     """Compile oracle.cpp -> liboracle.so (g++ -O2 -ffp-contract=off -fopenmp)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
         cmd = ["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
-               "-shared", "-o", _LIB + ".tmp", _SRC]
+               "-shared", "-o", tmp, _SRC]
         subprocess.run(cmd, check=True)
-        os.replace(_LIB + ".tmp", _LIB)
+        os.replace(tmp, _LIB)
     return _LIB
 
 

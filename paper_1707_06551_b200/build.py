@@ -23,7 +23,8 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     srcs = sources()
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(s) for s in srcs):
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", os.path.join(HERE, "csrc", "bie.cu")]
+    tmp = f"{LIB}.{os.getpid()}.tmp"  # per process: concurrent ranks may build at once
+    cmd = [NVCC, *FLAGS, "-o", tmp, os.path.join(HERE, "csrc", "bie.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{r.stdout}\n{r.stderr}")
@@ -31,7 +32,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
         fh.write(r.stderr)
     if verbose:
         print(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(tmp, LIB)  # atomic
     return LIB
 
 
