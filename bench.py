@@ -330,7 +330,9 @@ def CONFIG_DESC(c):
 
 # ------------------------------------------------------------------ CPU oracle
 def cpu_baseline(d, f_np, q_np, budget_s=15.0, kind="oracle"):
-    """Time the oracle (as it stands) on a bounded sample of the workload."""
+    """Time the oracle (as it stands) on a bounded random sample of the workload:
+    batches of random target nodes (and off-surface targets) are evaluated until
+    the time budget is spent; value = pairs evaluated / wall time."""
     import oracle
     oracle.build_oracle()
     cores = oracle.num_threads()
@@ -338,34 +340,31 @@ def cpu_baseline(d, f_np, q_np, budget_s=15.0, kind="oracle"):
     ns = nsn_of(d["p"])
     rng = np.random.default_rng(12345)
     has_off = d["targets"] is not None
-    share = 0.5 if has_off else 1.0
-
-    def timed_apply(nt):
-        sub = np.sort(rng.choice(N, nt, replace=False))
-        t0 = time.perf_counter()
-        oracle.apply(d["centres"], d["radii"], d["p"], d["mu"], f_np, q_np, sub)
-        return time.perf_counter() - t0, nt * (N - ns)
-
-    def timed_off(nt):
-        idx = np.sort(rng.choice(len(d["targets"]), nt, replace=False))
-        t0 = time.perf_counter()
-        oracle.offsurface(d["centres"], d["radii"], d["p"], d["mu"], f_np, q_np, d["targets"][idx])
-        return time.perf_counter() - t0, nt * N
-
-    probe = max(8, 2 * cores)
-    t, _ = timed_apply(probe)
-    nt = int(min(N, max(probe, probe * share * budget_s / max(t, 1e-3))))
-    ta, pa = timed_apply(nt)
-    tot_t, tot_p, desc = ta, pa, f"{nt} random nodes of the apply (far + self)"
-    if has_off:
-        t, _ = timed_off(probe)
-        mo = int(min(len(d["targets"]), max(probe, probe * share * budget_s / max(t, 1e-3))))
-        to, po_ = timed_off(mo)
-        tot_t += to
-        tot_p += po_
-        desc += f" + {mo} random off-surface targets"
+    legs = [("apply", N - ns, N)] + ([("off", N, len(d["targets"]))] if has_off else [])
+    share = budget_s / len(legs)
+    tot_t, tot_p, desc = 0.0, 0, []
+    for leg, pairs_per_target, pool in legs:
+        t_leg, n_leg, batch = 0.0, 0, max(8, 2 * cores)
+        while t_leg < share and n_leg < pool:
+            nt = int(min(batch, pool - n_leg))
+            t0 = time.perf_counter()
+            if leg == "apply":
+                sub = np.sort(rng.choice(N, nt, replace=False))
+                oracle.apply(d["centres"], d["radii"], d["p"], d["mu"], f_np, q_np, sub)
+            else:
+                idx = np.sort(rng.choice(pool, nt, replace=False))
+                oracle.offsurface(d["centres"], d["radii"], d["p"], d["mu"], f_np, q_np,
+                                  d["targets"][idx])
+            dt = time.perf_counter() - t0
+            t_leg += dt
+            n_leg += nt
+            rate = nt / max(dt, 1e-6)
+            batch = max(8, int(rate * (share - t_leg) * 1.05))
+        tot_t += t_leg
+        tot_p += n_leg * pairs_per_target
+        desc.append(f"{n_leg} random {'nodes of the apply (far + self)' if leg == 'apply' else 'off-surface targets'}")
     return {"value": tot_p / tot_t, "unit": "pair-interactions/s", "cores": cores, "kind": kind,
-            "sample": desc + f" of cfg, {tot_t:.1f} s wall"}
+            "sample": " + ".join(desc) + f" of cfg{d['cfg']}, {tot_t:.1f} s wall"}
 
 
 def run_reference(args):
