@@ -53,6 +53,7 @@ enum bie_status {
 /* Parts selector for bie_apply_parts (testing / measurement). */
 #define BIE_PART_FAR 1  /* smooth Nystrom sum over all other spheres (a3)  */
 #define BIE_PART_SELF 2 /* spectral self term (a4-a6)                     */
+#define BIE_PART_COMPLETION 4 /* completion L of eq 5.8 (bie_apply_K only)  */
 
 /* Kernel kinds reported by bie_get_profile. */
 #define BIE_KIND_SETUP 0    /* GL rule, Legendre/eigen tables, node generation (a1) */
@@ -65,7 +66,8 @@ enum bie_status {
 #define BIE_KIND_NEAR 7     /* near-singular correction (NEXT-1)              */
 #define BIE_KIND_KRYLOV 8   /* GMRES vector kernels (NEXT-2)                  */
 #define BIE_KIND_KFAR 9     /* far-field traction operator K pair sum (NEXT-3) */
-#define BIE_NUM_KINDS 10
+#define BIE_KIND_COMPLETE 10 /* completion operator L of eq 5.8 (NEXT-3)          */
+#define BIE_NUM_KINDS 11
 
 /*
  * bie_create -- build nodes, weights, normals and spectral tables (row a1).
@@ -140,8 +142,14 @@ int bie_apply_parts(bie_ctx* ctx, const double* f, const double* q, double* u, i
  * (reading R21: the adjoint of the R1 double layer, as P:219 requires),
  * smooth rule over every other sphere + the principal-value self term, whose
  * spectrum is that of D_pv (K_+ = D_-, K_- = D_+).  The one-sided
- * tractions are K_pv -+ sigma/2 (exterior: minus).  `parts` as in
- * bie_apply_parts.  The near correction (bie_set_near) does not apply to K.
+ * tractions are K_pv -+ sigma/2 (exterior: minus).  `parts`: bitwise OR of
+ * BIE_PART_FAR, BIE_PART_SELF and BIE_PART_COMPLETION (non-empty).  With
+ * BIE_PART_COMPLETION the completion operator of the mobility BIE (eq 5.8,
+ * P:490-491, "added ... to eliminate the 6n dimensional nullspace") is added:
+ *     L[sigma](x) = int_{G_s} sigma dG + (int_{G_s} (y - c_s) x sigma dG) x (x - c_s)
+ * for x on sphere s (reading R22: one rank-6 block per sphere, integrals by
+ * the node rule), so (1/2) sigma + u is the operator of eq 5.8's left side.
+ * The near correction (bie_set_near) does not apply to K.
  * sigma, u: device [N][3]; u must not overlap sigma.
  */
 int bie_apply_K(bie_ctx* ctx, const double* sigma, double* u, int parts, bie_stream_t s);

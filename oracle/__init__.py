@@ -305,6 +305,20 @@ def apply_K(centres, radii, p, sigma, subset=None):
             self_term(centres, radii, p, 1.0, None, sigma, subset))
 
 
+def completion(centres, radii, p, mu):
+    """Completion operator sum_k L_k[mu] of the mobility BIE (eq 5.8),
+    reading R22: block diagonal, one rank-6 block per sphere (all N nodes)."""
+    lib = _load_K()
+    if not getattr(lib, "_L_ready", False):
+        lib.oracle_completion.argtypes = [_DP, _DP, ctypes.c_int64, ctypes.c_int, _DP, _DP]
+        lib._L_ready = True
+    centres, radii, mu = _c(centres), _c(radii), _c(mu)
+    u = np.empty_like(mu)
+    if lib.oracle_completion(_dp(centres), _dp(radii), len(radii), p, _dp(mu), _dp(u)):
+        raise ValueError("completion: bad arguments")
+    return u
+
+
 def _load_near_off():
     lib = _load_near()
     if not getattr(lib, "_near_off_ready", False):

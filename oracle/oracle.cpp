@@ -737,6 +737,44 @@ extern "C" int oracle_K_at(const double* centres, const double* radii, int64_t n
   return 0;
 }
 
+// Completion operator of the mobility BIE (eq 5.8):
+//   L_k[mu](x) = int_{Gamma_k} mu dGamma
+//              + (int_{Gamma_k} (y - x_c) x mu(y) dGamma) x (x - x_c),
+// "added ... to eliminate the 6n dimensional nullspace of 1/2 I + K".  The
+// subscripts of eq 5.8 are garbled (x_i^c next to Gamma_k); reading R22: L_k
+// acts on the targets of its own body only (x in Gamma_k, x_c = x_k^c), so
+// sum_k L_k is block diagonal with one rank-6 block per sphere -- the only
+// reading that removes a 6n-dimensional (per-body rigid motion) nullspace
+// with per-body moments.  Integrals by the node rule (w of O-2), Neumaier.
+extern "C" int oracle_completion(const double* centres, const double* radii, int64_t ns, int p,
+                                 const double* mu, double* u) {
+  if (ns < 1 || p < 1 || !mu || !u) return 1;
+  Geometry G(centres, radii, ns, p);
+  for (int64_t s = 0; s < ns; ++s) {
+    const double* c = centres + 3 * s;
+    Neumaier F[3], T[3];
+    for (int64_t k = s * G.nsn; k < (s + 1) * G.nsn; ++k) {
+      const double d[3] = {G.x[3 * k] - c[0], G.x[3 * k + 1] - c[1], G.x[3 * k + 2] - c[2]};
+      const double* m = mu + 3 * k;
+      const double cr[3] = {d[1] * m[2] - d[2] * m[1], d[2] * m[0] - d[0] * m[2],
+                            d[0] * m[1] - d[1] * m[0]};
+      for (int e = 0; e < 3; ++e) {
+        F[e].add(G.w[k] * m[e]);
+        T[e].add(G.w[k] * cr[e]);
+      }
+    }
+    const double f[3] = {F[0].get(), F[1].get(), F[2].get()};
+    const double t[3] = {T[0].get(), T[1].get(), T[2].get()};
+    for (int64_t k = s * G.nsn; k < (s + 1) * G.nsn; ++k) {
+      const double d[3] = {G.x[3 * k] - c[0], G.x[3 * k + 1] - c[1], G.x[3 * k + 2] - c[2]};
+      u[3 * k + 0] = f[0] + (t[1] * d[2] - t[2] * d[1]);
+      u[3 * k + 1] = f[1] + (t[2] * d[0] - t[0] * d[2]);
+      u[3 * k + 2] = f[2] + (t[0] * d[1] - t[1] * d[0]);
+    }
+  }
+  return 0;
+}
+
 // ============================================ NEXT-1 for off-surface targets
 // Exterior pressure of a sphere's expansion: only the W_n channels carry
 // pressure outside (P:189 for S: n Y_n r^{-n-1}; the D value 2n(n-1) Y_n

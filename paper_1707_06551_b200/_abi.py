@@ -12,8 +12,8 @@ LIB_PATH = os.path.join(_HERE, "libbie.so")
 
 BIE_OK, BIE_ERR_ARG, BIE_ERR_GEOMETRY, BIE_ERR_ALLOC, BIE_ERR_CUDA, BIE_ERR_UNSUPPORTED = range(6)
 BIE_P_MAX = 30
-BIE_PART_FAR, BIE_PART_SELF = 1, 2
-KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov", "kfar")
+BIE_PART_FAR, BIE_PART_SELF, BIE_PART_COMPLETION = 1, 2, 4
+KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov", "kfar", "complete")
 BIE_NUM_KINDS = len(KINDS)
 
 #: every symbol include/bie.h declares (checked by tests/test_abi_cpu.py)
@@ -206,7 +206,8 @@ def bie_apply_parts(ctx, f, q, u, parts: int, stream=None):
 
 
 def bie_apply_K(ctx, sigma, u, parts=BIE_PART_FAR | BIE_PART_SELF, stream=None):
-    """u = K_pv[sigma] (traction operator, NEXT-3)."""
+    """u = K_pv[sigma] (traction operator, NEXT-3); with BIE_PART_COMPLETION in
+    `parts` also the completion L[sigma] of eq 5.8 (reading R22)."""
     N = bie_num_nodes(ctx)
     _check(ctx, _lib.bie_apply_K(ctx.handle, _ptr(sigma, device=True, n=3 * N),
                                  _ptr(u, device=True, n=3 * N), int(parts), _stream(stream)))

@@ -12,6 +12,7 @@
 
 #include "../../include/bie.h"
 #include "common.cuh"
+#include "k_complete.cuh"
 #include "k_krylov.cuh"
 #include "k_nbody.cuh"
 #include "k_near.cuh"
@@ -629,8 +630,8 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   if (!c) return BIE_ERR_ARG;
   int rc = check_device(c);
   if (rc) return rc;
-  if (parts <= 0 || parts > (BIE_PART_FAR | BIE_PART_SELF))
-    return fail(c, BIE_ERR_ARG, "parts must be a non-empty subset of FAR|SELF%s");
+  if (parts <= 0 || parts > (BIE_PART_FAR | BIE_PART_SELF | BIE_PART_COMPLETION))
+    return fail(c, BIE_ERR_ARG, "parts must be a non-empty subset of FAR|SELF|COMPLETION%s");
   const int64_t n3 = 3 * c->N;
   if (!sigma || !u || !is_device_ptr(sigma) || !is_device_ptr(u))
     return fail(c, BIE_ERR_ARG, "sigma and u must be device pointers%s");
@@ -656,8 +657,19 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   launch_self(SA, s);
   prof_end(c, s, &ev);
   rc = launch_check(c, "k_self");
-  if (rc || !(parts & BIE_PART_FAR)) return rc;
-  return run_far(c, u, s, 1);
+  if (rc) return rc;
+  if (parts & BIE_PART_FAR) {
+    rc = run_far(c, u, s, 1);
+    if (rc) return rc;
+  }
+  if (parts & BIE_PART_COMPLETION) {
+    prof_begin(c, BIE_KIND_COMPLETE, s, &ev);
+    k_completion<<<(unsigned)c->ns, kCompleteThreads, 0, s>>>(c->nsn, c->d_centres, c->d_x, c->d_w,
+                                                              sigma, u);
+    prof_end(c, s, &ev);
+    rc = launch_check(c, "k_completion");
+  }
+  return rc;
 }
 
 int bie_apply_SLDL(bie_ctx* c, const double* f, const double* q, double* u, bie_stream_t s) {

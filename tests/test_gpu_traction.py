@@ -54,3 +54,48 @@ def test_K_config3_subset(bie, oracle_mod):
     sub = d["subset"][::8]
     got = gpu_K(bie, d["centres"], d["radii"], d["p"], d["mu"], f)[sub]
     _assert_parity(got, oracle_mod.apply_K(d["centres"], d["radii"], d["p"], f, sub), "cfg3 K")
+
+
+@pytest.mark.parametrize("p,ns", [(3, 2), (6, 9), (12, 4), (30, 2)])
+def test_completion_matches_oracle(bie, oracle_mod, p, ns):
+    """Completion L of eq 5.8 (reading R22), alone and with K_pv; p = 30
+    exercises nsn = 1,922 > the CTA width (strided per-thread sums)."""
+    c, a, f, _, mu = _random_case(900 + p, ns, p, True, 1.3)
+    L = oracle_mod.completion(c, a, p, f)
+    _assert_parity(gpu_K(bie, c, a, p, mu, f, parts=bie.BIE_PART_COMPLETION), L, f"L p={p}")
+    full = gpu_K(bie, c, a, p, mu, f, parts=7)
+    _assert_parity(full, oracle_mod.apply_K(c, a, p, f) + L, f"K+L p={p}")
+
+
+def test_completion_rigid_closed_form_and_reproducible(bie, oracle_mod):
+    """L[F + W x (y - c)] = 4 pi a^2 F + (8 pi a^4/3) W x (x - c) on the device;
+    two launches agree bitwise (fixed-order moment reduction)."""
+    p = 10
+    c = np.array([[0.2, 0.1, -0.3], [3.5, 0.0, 0.4], [-1.0, 3.0, 0.0]])
+    a = np.array([1.1, 0.6, 0.9])
+    x, _, _ = oracle_mod.nodes(c, a, p)
+    nsn = (p + 1) * (2 * p + 2)
+    rng = np.random.default_rng(11)
+    F, W = rng.standard_normal((3, 3)), rng.standard_normal((3, 3))
+    sig = np.concatenate([F[b] + np.cross(W[b], x[b * nsn:(b + 1) * nsn] - c[b]) for b in range(3)])
+    ref = np.concatenate([4 * np.pi * a[b] ** 2 * F[b] +
+                          (8 * np.pi * a[b] ** 4 / 3) * np.cross(W[b], x[b * nsn:(b + 1) * nsn] - c[b])
+                          for b in range(3)])
+    g1 = gpu_K(bie, c, a, p, 1.0, sig, parts=bie.BIE_PART_COMPLETION)
+    g2 = gpu_K(bie, c, a, p, 1.0, sig, parts=bie.BIE_PART_COMPLETION)
+    assert np.abs(g1 - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert np.array_equal(g1, g2)
+
+
+def test_completion_part_only_for_K(bie):
+    """BIE_PART_COMPLETION belongs to bie_apply_K; bie_apply_parts rejects it."""
+    c = np.array([[0.0, 0.0, 0.0], [3.0, 0.0, 0.0]])
+    ctx = bie.bie_create(c, np.ones(2), 4, 1.0)
+    N = bie.bie_num_nodes(ctx)
+    x = torch.zeros(N, 3, dtype=torch.float64, device="cuda")
+    u = torch.empty_like(x)
+    with pytest.raises(bie.BieError):
+        bie.bie_apply_parts(ctx, x, x, u, bie.BIE_PART_COMPLETION)
+    with pytest.raises(bie.BieError):
+        bie.bie_apply_K(ctx, x, u, 8)
+    ctx.close()
