@@ -305,6 +305,47 @@ def apply_K(centres, radii, p, sigma, subset=None):
             self_term(centres, radii, p, 1.0, None, sigma, subset))
 
 
+def _load_near_K():
+    lib = _load_K()
+    if not getattr(lib, "_nearK_ready", False):
+        i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        lib.oracle_exterior_traction.argtypes = [i32, _DP, d, _DP, _DP, _DP, i64, _DP]
+        lib.oracle_near_K.argtypes = [_DP, _DP, i64, i32, _DP, d, _I64P, i64, _DP]
+        lib._nearK_ready = True
+    return lib
+
+
+def exterior_traction(p, centre, a, sigma_s, targets, normals):
+    """Traction (K) of ONE sphere's degree-<=p single-layer expansion at exterior
+    points with given unit normals (eqs 3.17-3.18, reading R24)."""
+    lib = _load_near_K()
+    centre, sigma_s, targets, normals = _c(centre), _c(sigma_s), _c(targets), _c(normals)
+    t = np.empty((targets.shape[0], 3))
+    if lib.oracle_exterior_traction(p, _dp(centre), float(a), _dp(sigma_s), _dp(targets),
+                                    _dp(normals), targets.shape[0], _dp(t)):
+        raise ValueError("exterior_traction: bad arguments")
+    return t
+
+
+def near_K(centres, radii, p, sigma, eta, subset=None):
+    """Near correction of K at nodes (eq 4.5 partition): exterior traction minus
+    the smooth-rule K sum, over the near spheres."""
+    lib = _load_near_K()
+    centres, radii, sigma = _c(centres), _c(radii), _c(sigma)
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    idx = _subset(subset, N)
+    du = np.empty((len(idx), 3))
+    if lib.oracle_near_K(_dp(centres), _dp(radii), len(radii), p, _dp(sigma), float(eta),
+                         idx.ctypes.data_as(_I64P), len(idx), _dp(du)):
+        raise ValueError("near_K: bad arguments")
+    return du
+
+
+def apply_K_near(centres, radii, p, sigma, eta, subset=None):
+    """K_pv with the near-singular correction: apply_K + near_K."""
+    return apply_K(centres, radii, p, sigma, subset) + near_K(centres, radii, p, sigma, eta, subset)
+
+
 def completion(centres, radii, p, mu):
     """Completion operator sum_k L_k[mu] of the mobility BIE (eq 5.8),
     reading R22: block diagonal, one rank-6 block per sphere (all N nodes)."""

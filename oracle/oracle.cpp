@@ -737,6 +737,142 @@ extern "C" int oracle_K_at(const double* centres, const double* radii, int64_t n
   return 0;
 }
 
+// ----------------------------------------------- NEXT-3: near correction for K
+// Traction of the exterior single-layer flow of ONE sphere: the
+// field is the expansion of eqs 3.6-3.8 (eq 3.17: each term u = g(r) Z with Z
+// in {V, W, X}); PAPER eq 3.18 gives the traction of one term,
+//   (grad u + grad u^T - pI) n = g'(r) ((e_r.n) Z + (Z.n) e_r)
+//                              + (g(r)/r) (grad_g Z + grad_g Z^T) n - q(r) Y n,
+// with grad_g Z the surface gradient of Z's Cartesian components on the unit
+// sphere (hence the 1/r at radius r) and p = q(r) Y_n^m the pressure of the
+// S[W_n^m] term (n Y r^{-n-1}).  Eq 3.18 prints "+ q Y n"; the
+// Newtonian stress -pI gives "- q Y n" (reading R24).  Unit sphere, mu = 1:
+// K is a- and mu-free (the a/mu of S and the 1/a of grad cancel).  The
+// surface derivatives are written out in spherical coordinates with the
+// Legendre equation for Y_thth, so targets on the source's polar axis
+// (sin theta = 0) are excluded from this routine (the tests avoid them).
+static void exterior_traction(int p, const double* c, double a, const std::vector<cplx>& al,
+                              const double* x, const double* nv, double out[3]) {
+  const double rv[3] = {(x[0] - c[0]) / a, (x[1] - c[1]) / a, (x[2] - c[2]) / a};
+  const double r = std::sqrt(rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2]);
+  const double th = std::acos(rv[2] / r), ph = std::atan2(rv[1], rv[0]);
+  const double st = std::sin(th), ct = std::cos(th), sp = std::sin(ph), cp = std::cos(ph);
+  const double er[3] = {st * cp, st * sp, ct}, et[3] = {ct * cp, ct * sp, -st}, ep[3] = {-sp, cp, 0.0};
+  const double nr = er[0] * nv[0] + er[1] * nv[1] + er[2] * nv[2];
+  const double nt = et[0] * nv[0] + et[1] * nv[1] + et[2] * nv[2];
+  const double np = ep[0] * nv[0] + ep[1] * nv[1] + ep[2] * nv[2];
+  const double cot = ct / st;
+  const cplx I(0.0, 1.0);
+  cplx acc[3] = {0.0, 0.0, 0.0};
+  // one term g Z (value Z, theta-derivative Zt, (1/sin th) phi-derivative Zp)
+  auto term = [&](cplx coef, double g, double gp, const cplx* Z, const cplx* Zt, const cplx* Zp) {
+    cplx Zn = 0.0, Ztn = 0.0, Zpn = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      Zn += Z[k] * nv[k];
+      Ztn += Zt[k] * nv[k];
+      Zpn += Zp[k] * nv[k];
+    }
+    for (int k = 0; k < 3; ++k)
+      acc[k] += coef * (gp * (nr * Z[k] + Zn * er[k]) +
+                        (g / r) * (Zt[k] * nt + Zp[k] * np + et[k] * Ztn + ep[k] * Zpn));
+  };
+  for (int n = 1; n <= p; ++n)
+    for (int m = -n; m <= n; ++m) {
+      cplx Y, A, B;
+      ynm_all(n, m, th, ph, &Y, &A, &B);  // Y, Y_th, (1/st) Y_ph
+      const double mm = (double)m;
+      const cplx At = -cot * A - (n * (n + 1.0) - mm * mm / (st * st)) * Y;  // Legendre eq.
+      const cplx Bt = (I * mm / st) * (A - cot * Y);
+      const cplx Ap = (I * mm / st) * A, Bp = (I * mm / st) * B;
+      cplx V[3], Vt[3], Vp[3], W[3], Wt[3], Wp[3], X[3], Xt[3], Xp[3];
+      for (int k = 0; k < 3; ++k) {
+        const cplx Yr = Y * er[k], Yrt = A * er[k] + Y * et[k], Yrp = B * er[k] + Y * ep[k];
+        const cplx G = A * et[k] + B * ep[k];
+        const cplx Gt = At * et[k] - A * er[k] + Bt * ep[k];
+        const cplx Gp = Ap * et[k] + A * cot * ep[k] + Bp * ep[k] - B * (er[k] + cot * et[k]);
+        V[k] = G - (n + 1.0) * Yr;  Vt[k] = Gt - (n + 1.0) * Yrt;  Vp[k] = Gp - (n + 1.0) * Yrp;
+        W[k] = G + (double)n * Yr;  Wt[k] = Gt + (double)n * Yrt;  Wp[k] = Gp + (double)n * Yrp;
+        X[k] = A * ep[k] - B * et[k];
+        Xt[k] = At * ep[k] - Bt * et[k] + B * er[k];
+        Xp[k] = Ap * ep[k] - A * (er[k] + cot * et[k]) - Bp * et[k] - B * cot * ep[k];
+      }
+      const size_t ix = (size_t)(n * n + n + m) * 3;
+      const double d = 2.0 * n + 1.0;
+      const double rn2 = std::pow(r, -n - 2.0), rn = std::pow(r, -(double)n), rn1 = std::pow(r, -n - 1.0);
+      // S[V] = n/(d(2n+3)) V r^{-n-2}                                  (eq 3.6)
+      const double cV = n / (d * (2.0 * n + 3.0));
+      term(al[ix], cV * rn2, -(n + 2.0) * cV * rn2 / r, V, Vt, Vp);
+      // S[W] = (n+1)/(d(2n-1)) W r^{-n} + n/(4n+2) V (r^{-n-2} - r^{-n}) (eq 3.7)
+      const double cW = (n + 1.0) / (d * (2.0 * n - 1.0)), cWV = n / (4.0 * n + 2.0);
+      term(al[ix + 1], cW * rn, -n * cW * rn / r, W, Wt, Wp);
+      term(al[ix + 1], cWV * (rn2 - rn), cWV * (-(n + 2.0) * rn2 + n * rn) / r, V, Vt, Vp);
+      // S[X] = 1/d X r^{-n-1}                                          (eq 3.8)
+      term(al[ix + 2], rn1 / d, -(n + 1.0) * rn1 / (d * r), X, Xt, Xp);
+      // pressure of S[W]: n Y r^{-n-1}, traction -p n
+      const cplx pq = al[ix + 1] * (double)n * Y * rn1;
+      for (int k = 0; k < 3; ++k) acc[k] -= pq * nv[k];
+    }
+  for (int k = 0; k < 3; ++k) out[k] = acc[k].real();
+}
+
+extern "C" int oracle_exterior_traction(int p, const double* c, double a, const double* sigma_s,
+                                        const double* targets, const double* normals, int64_t m,
+                                        double* t) {
+  if (p < 1 || !(a > 0) || !c || !sigma_s || (m > 0 && (!targets || !normals || !t))) return 1;
+  std::vector<cplx> al;
+  project_sphere(p, sigma_s, al);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < m; ++i) exterior_traction(p, c, a, al, targets + 3 * i, normals + 3 * i, t + 3 * i);
+  return 0;
+}
+
+// Near correction of K at the subset nodes tidx (eq 4.5 partition, as
+// oracle_near): dK_i = sum over near spheres s of [exterior traction of s at
+// x_i with normal n_i  -  smooth-rule K sum over s's nodes].
+extern "C" int oracle_near_K(const double* centres, const double* radii, int64_t ns, int p,
+                             const double* sigma, double eta, const int64_t* tidx, int64_t nt,
+                             double* du) {
+  if (ns < 1 || p < 1 || !sigma || !(eta >= 0) || !du || !tidx) return 1;
+  Geometry G(centres, radii, ns, p);
+  const int nsn = G.nsn;
+  std::vector<char> need(ns, 0);
+  for (int64_t q = 0; q < nt; ++q) {
+    const int64_t t = tidx[q] / nsn;
+    for (int64_t s = 0; s < ns; ++s)
+      if (s != t && oracle_is_near(centres + 3 * s, radii[s], centres + 3 * t, radii[t], eta)) need[s] = 1;
+  }
+  std::vector<std::vector<cplx>> AL(ns);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = 0; s < ns; ++s)
+    if (need[s]) project_sphere(p, sigma + 3 * s * nsn, AL[s]);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t q = 0; q < nt; ++q) {
+    const int64_t i = tidx[q], t = i / nsn;
+    const double* x = &G.x[3 * i];
+    const double* nx = &G.n[3 * i];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t s = 0; s < ns; ++s) {
+      if (s == t || !oracle_is_near(centres + 3 * s, radii[s], centres + 3 * t, radii[t], eta)) continue;
+      double te[3];
+      exterior_traction(p, centres + 3 * s, radii[s], AL[s], x, nx, te);
+      Neumaier sm[3];
+      for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
+        const double* y = &G.x[3 * k];
+        const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
+        const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
+        const double r5 = r2 * r2 * std::sqrt(r2);
+        const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
+        const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
+        const double cK = -3.0 * G.w[k] / (4.0 * PI);
+        for (int e = 0; e < 3; ++e) sm[e].add(cK * rn * rs * rho[e] / r5);
+      }
+      for (int e = 0; e < 3; ++e) acc[e] += te[e] - sm[e].get();
+    }
+    for (int e = 0; e < 3; ++e) du[3 * q + e] = acc[e];
+  }
+  return 0;
+}
+
 // Completion operator of the mobility BIE (eq 5.8):
 //   L_k[mu](x) = int_{Gamma_k} mu dGamma
 //              + (int_{Gamma_k} (y - x_c) x mu(y) dGamma) x (x - x_c),
