@@ -149,7 +149,10 @@ int bie_apply_parts(bie_ctx* ctx, const double* f, const double* q, double* u, i
  *     L[sigma](x) = int_{G_s} sigma dG + (int_{G_s} (y - c_s) x sigma dG) x (x - c_s)
  * for x on sphere s (reading R22: one rank-6 block per sphere, integrals by
  * the node rule), so (1/2) sigma + u is the operator of eq 5.8's left side.
- * The near correction (bie_set_near) does not apply to K.
+ * With bie_set_near(eta > 0) and BIE_PART_FAR, sphere pairs failing eq 4.5
+ * get the traction of the source sphere's exact degree-<=p single-layer
+ * expansion instead of the smooth rule (eqs 3.17-3.18; reading
+ * R24), evaluated at the target node with the target normal.
  * sigma, u: device [N][3]; u must not overlap sigma.
  */
 int bie_apply_K(bie_ctx* ctx, const double* sigma, double* u, int parts, bie_stream_t s);

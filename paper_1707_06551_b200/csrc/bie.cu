@@ -16,6 +16,7 @@
 #include "k_krylov.cuh"
 #include "k_nbody.cuh"
 #include "k_near.cuh"
+#include "k_near_K.cuh"
 #include "k_self.cuh"
 #include "k_setup.cuh"
 
@@ -567,6 +568,10 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
                        (int)(near_smem_doubles(p, true) * sizeof(double)));
   cudaFuncSetAttribute(k_near<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p, false) * sizeof(double)));
+  cudaFuncSetAttribute(k_near_K<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_smem_doubles(p, true) * sizeof(double)));
+  cudaFuncSetAttribute(k_near_K<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_smem_doubles(p, false) * sizeof(double)));
   cudaFuncSetAttribute(k_near_off<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_off_smem_doubles(p) * sizeof(double)));
   cudaFuncSetAttribute(k_near_off<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -650,7 +655,8 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   SA.u = u;
   SA.rec = c->d_rec;
   SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
-  SA.alpha = nullptr;
+  const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
+  SA.alpha = near ? c->d_alpha : nullptr;  // projections of sigma (q slot)
   SA.precond = 0;
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
@@ -659,8 +665,39 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   rc = launch_check(c, "k_self");
   if (rc) return rc;
   if (parts & BIE_PART_FAR) {
+    if (near) {
+      const TableLayout L(c->p);
+      const int64_t n = c->ns * L.nlm;
+      prof_begin(c, BIE_KIND_NEAR, s, &ev);
+      k_near_coef_K<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(c->p, c->ns, c->d_alpha, c->d_ncoef);
+      prof_end(c, s, &ev);
+      rc = launch_check(c, "k_near_coef_K");
+      if (rc) return rc;
+    }
     rc = run_far(c, u, s, 1);
     if (rc) return rc;
+    if (near) {  // traction of the exact exterior expansion for near pairs
+      NearArgs NA;
+      NA.p = c->p;
+      NA.nsn = c->nsn;
+      NA.tab = c->d_tab;
+      NA.centres = c->d_centres;
+      NA.radii = c->d_radii;
+      NA.rec = c->d_rec;
+      NA.coef = c->d_ncoef;
+      NA.tgt = c->d_near_tgt;
+      NA.nb_off = c->d_nb_off;
+      NA.nb_idx = c->d_nb_idx;
+      NA.u = u;
+      prof_begin(c, BIE_KIND_NEAR, s, &ev);
+      const bool stage = near_stage(c->p);
+      const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
+      if (stage) k_near_K<true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+      else k_near_K<false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+      prof_end(c, s, &ev);
+      rc = launch_check(c, "k_near_K");
+      if (rc) return rc;
+    }
   }
   if (parts & BIE_PART_COMPLETION) {
     prof_begin(c, BIE_KIND_COMPLETE, s, &ev);

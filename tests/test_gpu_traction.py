@@ -99,3 +99,56 @@ def test_completion_part_only_for_K(bie):
     with pytest.raises(bie.BieError):
         bie.bie_apply_K(ctx, x, u, 8)
     ctx.close()
+
+
+# ---------------------------------------------- near-singular correction of K
+def gpu_K_near(bie, c, a, p, mu, sigma, eta, parts=3):
+    ctx = bie.bie_create(c, a, p, mu)
+    bie.bie_set_near(ctx, eta)
+    u = torch.full((len(sigma), 3), np.nan, dtype=torch.float64, device="cuda")
+    bie.bie_apply_K(ctx, _dev(sigma), u, parts)
+    torch.cuda.synchronize()
+    ctx.close()
+    return u.cpu().numpy()
+
+
+@pytest.mark.parametrize("p,ns,eta", [(4, 6, 1.0), (6, 8, 2.0), (8, 5, 0.7), (12, 4, 1.0), (3, 10, 3.0)])
+def test_K_near_matches_oracle(bie, oracle_mod, p, ns, eta):
+    c, a, f, _, mu = _random_case(1100 + p, ns, p, True, 0.9)
+    ref = oracle_mod.apply_K_near(c, a, p, f, eta)
+    _assert_parity(gpu_K_near(bie, c, a, p, mu, f, eta), ref, f"K near p={p} eta={eta}")
+    if p == 6:  # with the completion operator as well
+        _assert_parity(gpu_K_near(bie, c, a, p, mu, f, eta, parts=7),
+                       ref + oracle_mod.completion(c, a, p, f), "K near + L")
+
+
+def test_K_near_config3_subset(bie, oracle_mod):
+    from tests.test_gpu_parity import _cfg_inputs
+    d, f, _ = _cfg_inputs(oracle_mod, 3)
+    sub = d["subset"][::8]
+    got = gpu_K_near(bie, d["centres"], d["radii"], d["p"], d["mu"], f, 1.0)[sub]
+    ref = oracle_mod.apply_K_near(d["centres"], d["radii"], d["p"], f, 1.0, sub)
+    _assert_parity(got, ref, "cfg3 K near")
+
+
+@pytest.mark.parametrize("direction", [(0.0, 0.0, 1.0), (0.3, -0.5, 0.8)])
+def test_K_near_two_spheres_vs_converged_quadrature(bie, oracle_mod, direction):
+    """Independent of the oracle's derivative formulas: two spheres at gap 0.5
+    (axis-aligned and oblique) with band-limited densities; the near-corrected
+    K_pv at sphere 0's nodes == sphere 0's self term + the converged (p = 96
+    fine grid) K integral over sphere 1, to 1e-12."""
+    from tests.test_oracle_near_K import _bandlimited
+    p = 8
+    e = np.array(direction) / np.linalg.norm(direction)
+    a = np.array([1.0, 0.9])
+    c = np.stack([np.zeros(3), (a[0] + a[1] + 0.5) * e])
+    x, nrm, _ = oracle_mod.nodes(c, a, p)
+    nsn = (p + 1) * (2 * p + 2)
+    sig = np.concatenate([_bandlimited(21, p, x[:nsn], c[0], a[0]),
+                          _bandlimited(22, p, x[nsn:], c[1], a[1])])
+    got = gpu_K_near(bie, c, a, p, 1.0, sig, 1.0)[:nsn]
+    xf, _, _ = oracle_mod.nodes(c[1:], a[1:], 96)
+    sigf = _bandlimited(22, p, xf, c[1], a[1])
+    ref = (oracle_mod.self_term(c, a, p, 1.0, None, sig, np.arange(nsn)) +
+           oracle_mod.K_at(c[1:], a[1:], 96, sigf, x[:nsn], nrm[:nsn]))
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
