@@ -32,9 +32,21 @@ def main():
         prof = bie.bie_get_profile(ctx)
         ms = prof["kfar"][0] / reps
         pairs = N * (N - nsn)
-        print(json.dumps({"config": cfg, "pairs": pairs, "kfar_ms": ms, "pairs_per_s": pairs / (ms / 1e3),
-                          "fp64_pipe_frac": pairs / (ms / 1e3) * 25 / (148 * 64 * 1.965e9),
-                          "apply_K_ms": sum(v[0] for v in prof.values()) / reps}), flush=True)
+        rec = {"config": cfg, "pairs": pairs, "kfar_ms": ms, "pairs_per_s": pairs / (ms / 1e3),
+               "fp64_pipe_frac": pairs / (ms / 1e3) * 25 / (148 * 64 * 1.965e9),
+               "apply_K_ms": sum(v[0] for v in prof.values()) / reps}
+        # near-singular correction (eta = 1) and the completion operator L (eq 5.8)
+        bie.bie_set_near(ctx, 1.0)
+        bie.bie_apply_K(ctx, S, U, 7)
+        torch.cuda.synchronize()
+        bie.bie_reset_profile(ctx)
+        for _ in range(reps):
+            bie.bie_apply_K(ctx, S, U, 7)
+        prof = bie.bie_get_profile(ctx)
+        rec.update({"near_pairs_eta1": bie.bie_near_pairs(ctx), "near_K_ms": prof["near"][0] / reps,
+                    "completion_ms": prof["complete"][0] / reps,
+                    "apply_K_near_L_ms": sum(v[0] for v in prof.values()) / reps})
+        print(json.dumps(rec), flush=True)
         ctx.close()
 
 

@@ -3,7 +3,8 @@
   --what K      : bie_apply_K on cfg 3           (k_nbody MODE=1)
   --what near   : apply with eta = 1 on cfg 4    (k_near, k_near_coef)
   --what nearoff: off-surface with eta = 1, cfg 5, 200k targets (k_near_off)
-  --what self   : self term only, cfg 5          (k_self_t)"""
+  --what self   : self term only, cfg 5          (k_self_t)
+  --what nearK  : K apply with eta = 1 on cfg 4   (k_near_K, k_near_coef_K)"""
 import argparse
 import os
 import sys
@@ -21,7 +22,7 @@ def main():
     import torch
     import paper_1707_06551_b200 as bie
     from bie_inputs import make_config
-    cfg = {"K": 3, "near": 4, "nearoff": 5, "self": 5}[a.what]
+    cfg = {"K": 3, "near": 4, "nearoff": 5, "self": 5, "nearK": 4}[a.what]
     d = make_config(cfg, with_targets=(a.what == "nearoff"))
     ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
     N = d["n_nodes"]
@@ -30,6 +31,9 @@ def main():
     Q = torch.from_numpy(g.standard_normal((N, 3))).cuda()
     U = torch.empty_like(F)
     if a.what == "K":
+        bie.bie_apply_K(ctx, F, U)
+    elif a.what == "nearK":
+        bie.bie_set_near(ctx, 1.0)
         bie.bie_apply_K(ctx, F, U)
     elif a.what == "near":
         bie.bie_set_near(ctx, 1.0)
