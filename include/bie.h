@@ -173,6 +173,24 @@ int bie_eval_offsurface(bie_ctx* ctx, const double* f, const double* q, const do
                         int64_t m, double* u, double* p, bie_stream_t s);
 
 /*
+ * bie_eval_traction -- traction of the single-layer flow S[sigma] at m
+ * arbitrary points with given normals (eq 2.22 off the
+ * surface, whose one-sphere closed forms are eqs 3.19-3.21):
+ *   t(x) = K[sigma](x; n) = (grad u + grad u^T - pI) n,  u = S[sigma],
+ *        = -(3/(4 pi)) sum_k w_k ((x-y_k).n)((x-y_k).sigma_k)(x-y_k)/|x-y_k|^5
+ * (smooth rule over ALL nodes; mu- and a-free).  With bie_set_near(eta > 0)
+ * a target at point-to-surface distance 0 <= d < eta 2 a_s from sphere s
+ * gets the traction of s's exact degree-<=p expansion instead of s's smooth
+ * sum (eqs 3.17-3.18, reading R24; exterior targets only, as
+ * bie_eval_offsurface).  sigma: device [N][3]; targets, normals, t: device
+ * [m][3]; normals are used as given (unit length expected, not
+ * renormalised).  m = 0 is a no-op; a target on a node gives inf/NaN.
+ * Uses the context's packed-source scratch, like every apply.
+ */
+int bie_eval_traction(bie_ctx* ctx, const double* sigma, const double* targets,
+                      const double* normals, int64_t m, double* t, bie_stream_t s);
+
+/*
  * Host-buffer variants (end-to-end): identical results; the inputs are copied
  * host->device on s (pinned host memory makes the copies asynchronous), the
  * outputs device->host, and the call synchronises s before returning.

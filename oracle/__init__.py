@@ -346,6 +346,28 @@ def apply_K_near(centres, radii, p, sigma, eta, subset=None):
     return apply_K(centres, radii, p, sigma, subset) + near_K(centres, radii, p, sigma, eta, subset)
 
 
+def traction_offsurface(centres, radii, p, sigma, targets, normals, eta=0.0):
+    """K[sigma] at arbitrary points with given normals: smooth rule over every
+    node (K_at) + the near correction for exterior targets within eta 2 a_s of
+    a sphere's surface (exterior traction of its expansion, eqs 3.17-3.18)."""
+    lib = _load_near_K()
+    if not getattr(lib, "_nearKoff_ready", False):
+        i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        lib.oracle_near_K_offsurface.argtypes = [_DP, _DP, i64, i32, _DP, d, _DP, _DP, i64, _DP]
+        lib._nearKoff_ready = True
+    t = K_at(centres, radii, p, sigma, targets, normals)
+    if eta > 0:
+        centres, radii, sigma, targets, normals = (_c(centres), _c(radii), _c(sigma), _c(targets),
+                                                   _c(normals))
+        dt = np.empty_like(t)
+        if lib.oracle_near_K_offsurface(_dp(centres), _dp(radii), len(radii), p, _dp(sigma),
+                                        float(eta), _dp(targets), _dp(normals), targets.shape[0],
+                                        _dp(dt)):
+            raise ValueError("traction_offsurface: bad arguments")
+        t = t + dt
+    return t
+
+
 def completion(centres, radii, p, mu):
     """Completion operator sum_k L_k[mu] of the mobility BIE (eq 5.8),
     reading R22: block diagonal, one rank-6 block per sphere (all N nodes)."""

@@ -873,6 +873,58 @@ extern "C" int oracle_near_K(const double* centres, const double* radii, int64_t
   return 0;
 }
 
+// Near correction of K at arbitrary targets with given normals: target x and
+// sphere s are near when 0 <= |x - c_s| - a_s < eta 2 a_s (as
+// oracle_near_offsurface; exterior targets only).  dt = sum over near s of
+// [exterior traction of s  -  smooth-rule K sum over s's nodes].  The
+// corrected evaluator is oracle_K_at + this.
+extern "C" int oracle_near_K_offsurface(const double* centres, const double* radii, int64_t ns,
+                                        int p, const double* sigma, double eta,
+                                        const double* targets, const double* normals, int64_t m,
+                                        double* dt) {
+  if (ns < 1 || p < 1 || !sigma || !(eta >= 0) || (m > 0 && (!targets || !normals || !dt))) return 1;
+  Geometry G(centres, radii, ns, p);
+  const int nsn = G.nsn;
+  auto near_pt = [&](int64_t s, const double* x) {
+    const double dx = x[0] - centres[3 * s], dy = x[1] - centres[3 * s + 1], dz = x[2] - centres[3 * s + 2];
+    const double d = std::sqrt(dx * dx + dy * dy + dz * dz) - radii[s];
+    return d >= 0.0 && d < eta * 2.0 * radii[s];
+  };
+  std::vector<char> need(ns, 0);
+  for (int64_t t = 0; t < m; ++t)
+    for (int64_t s = 0; s < ns; ++s)
+      if (near_pt(s, targets + 3 * t)) need[s] = 1;
+  std::vector<std::vector<cplx>> AL(ns);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = 0; s < ns; ++s)
+    if (need[s]) project_sphere(p, sigma + 3 * s * nsn, AL[s]);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < m; ++t) {
+    const double* x = targets + 3 * t;
+    const double* nx = normals + 3 * t;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t s = 0; s < ns; ++s) {
+      if (!near_pt(s, x)) continue;
+      double te[3];
+      exterior_traction(p, centres + 3 * s, radii[s], AL[s], x, nx, te);
+      Neumaier sm[3];
+      for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
+        const double* y = &G.x[3 * k];
+        const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
+        const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
+        const double r5 = r2 * r2 * std::sqrt(r2);
+        const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
+        const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
+        const double cK = -3.0 * G.w[k] / (4.0 * PI);
+        for (int e = 0; e < 3; ++e) sm[e].add(cK * rn * rs * rho[e] / r5);
+      }
+      for (int e = 0; e < 3; ++e) acc[e] += te[e] - sm[e].get();
+    }
+    for (int e = 0; e < 3; ++e) dt[3 * t + e] = acc[e];
+  }
+  return 0;
+}
+
 // Completion operator of the mobility BIE (eq 5.8):
 //   L_k[mu](x) = int_{Gamma_k} mu dGamma
 //              + (int_{Gamma_k} (y - x_c) x mu(y) dGamma) x (x - x_c),

@@ -22,7 +22,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
-    "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K",
+    "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K", "bie_eval_traction",
     "bie_status_string", "bie_last_error",
 )
 
@@ -57,6 +57,7 @@ _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
 _lib.bie_near_pairs.restype = _i64
 _lib.bie_apply_K.argtypes = [_vp, _vp, _vp, _i32, _vp]
+_lib.bie_eval_traction.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
 _lib.bie_solve_porous.argtypes = [_vp, _vp, _vp, _d, _i32, _i32, _i32, ctypes.POINTER(_i32),
                                   ctypes.POINTER(_d), _vp]
 _lib.bie_status_string.argtypes = [_i32]
@@ -211,6 +212,16 @@ def bie_apply_K(ctx, sigma, u, parts=BIE_PART_FAR | BIE_PART_SELF, stream=None):
     N = bie_num_nodes(ctx)
     _check(ctx, _lib.bie_apply_K(ctx.handle, _ptr(sigma, device=True, n=3 * N),
                                  _ptr(u, device=True, n=3 * N), int(parts), _stream(stream)))
+
+
+def bie_eval_traction(ctx, sigma, targets, normals, t, stream=None):
+    """t = K[sigma](x; n) at arbitrary targets with normals (NEXT-3 off the surface)."""
+    N = bie_num_nodes(ctx)
+    m = (targets.numel() if hasattr(targets, "numel") else targets.size) // 3
+    _check(ctx, _lib.bie_eval_traction(ctx.handle, _ptr(sigma, device=True, n=3 * N),
+                                       _ptr(targets, device=True, n=3 * m),
+                                       _ptr(normals, device=True, n=3 * m), m,
+                                       _ptr(t, device=True, n=3 * m), _stream(stream)))
 
 
 def bie_eval_offsurface(ctx, f, q, targets, u, p=None, stream=None):

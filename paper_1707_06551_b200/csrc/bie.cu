@@ -36,6 +36,7 @@ constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 #define NBODY_APPLY k_nbody<kR, kTPB, kTS, kNST, false, 1, 2>
 #define NBODY_OFF k_nbody<kR, kTPB, kTS, kNST, true, 1, 1>
 #define NBODY_K k_nbody<kR, kTPB, kTS, kNST, false, 1, 2, 1>
+#define NBODY_OFFK k_nbody<kR, kTPB, kTS, kNST, true, 1, 1, 1>
 
 struct Ev {
   int kind;
@@ -45,7 +46,7 @@ struct Ev {
 }  // namespace
 
 struct bie_ctx {
-  int dev = -1, sm_count = 0, occ_apply = 1, occ_off = 1, occ_K = 1;
+  int dev = -1, sm_count = 0, occ_apply = 1, occ_off = 1, occ_K = 1, occ_offK = 1;
   int p = 0, nsn = 0;
   int64_t ns = 0, N = 0;
   double mu = 1.0;
@@ -461,6 +462,106 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   return launch_check(c, "k_near_off");
 }
 
+// NEXT-3 off the surface: traction K[sigma](x; n) at m targets with normals
+static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const double* tn,
+                        int64_t m, double* t, cudaStream_t s) {
+  Ev ev;
+  int rc;
+  const bool near = c->eta > 0.0 && c->d_alpha;
+  if (near) {  // projections of sigma (q slot) -> exterior S coefficients
+    SelfArgs SA;
+    SA.p = c->p;
+    SA.ns = c->ns;
+    SA.mu = c->mu;
+    SA.tab = c->d_tab;
+    SA.centres = c->d_centres;
+    SA.radii = c->d_radii;
+    SA.f = nullptr;
+    SA.q = sigma;
+    SA.u = nullptr;
+    SA.rec = c->d_rec;
+    SA.self = 0;
+    SA.alpha = c->d_alpha;
+    SA.precond = 0;
+    prof_begin(c, BIE_KIND_SELF, s, &ev);
+    launch_self(SA, s);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_self"))) return rc;
+    const TableLayout L(c->p);
+    const int64_t n = c->ns * L.nlm;
+    prof_begin(c, BIE_KIND_NEAR, s, &ev);
+    k_near_coef_K<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(c->p, c->ns, c->d_alpha, c->d_ncoef);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_near_coef_K"))) return rc;
+  }
+  prof_begin(c, BIE_KIND_PACK, s, &ev);  // q' = (3/4pi) w sigma
+  k_pack<<<(unsigned)((c->N + 255) / 256), 256, 0, s>>>(c->p, c->N, c->mu, c->d_tab, c->d_centres,
+                                                        c->d_radii, nullptr, sigma, c->d_rec, c->d_qn3);
+  prof_end(c, s, &ev);
+  if ((rc = launch_check(c, "k_pack"))) return rc;
+  const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
+  for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
+    const int64_t Mb = std::min(kOffBatch, m - b0);
+    const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_offK);
+    NbodyArgs A;
+    A.rec = c->d_rec;
+    A.qn3 = nullptr;
+    A.tx = tg + 3 * b0;
+    A.tn = tn + 3 * b0;
+    A.uinit = nullptr;
+    A.pout = nullptr;
+    A.N = c->N;
+    A.M = Mb;
+    A.nsn = c->nsn;
+    A.n_tt = P.n_tt;
+    A.n_chunks = P.n_chunks;
+    A.tiles_per_chunk = P.tiles_per_chunk;
+    A.pscale = 0.0;
+    if (P.n_chunks == 1) {
+      A.uout = t + 3 * b0;
+      prof_begin(c, BIE_KIND_KFAR, s, &ev);
+      NBODY_OFFK<<<(unsigned)P.n_tt, kTPB, nb_smem, s>>>(A);
+      prof_end(c, s, &ev);
+      if ((rc = launch_check(c, "k_nbody_offK"))) return rc;
+      continue;
+    }
+    if ((rc = ensure_part(c, (size_t)P.n_chunks * 4 * Mb))) return rc;
+    A.uout = c->d_part;
+    prof_begin(c, BIE_KIND_KFAR, s, &ev);
+    NBODY_OFFK<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_nbody_offK"))) return rc;
+    prof_begin(c, BIE_KIND_REDUCE, s, &ev);
+    k_reduce<<<(unsigned)((3 * Mb + 255) / 256), 256, 0, s>>>(Mb, P.n_chunks, c->d_part, nullptr,
+                                                                t + 3 * b0, nullptr, nullptr, 0.0);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_reduce"))) return rc;
+  }
+  if (!near) return BIE_OK;
+  NearOffArgs NO;
+  NO.p = c->p;
+  NO.nsn = c->nsn;
+  NO.ns = c->ns;
+  NO.M = m;
+  NO.mu = c->mu;
+  NO.eta = c->eta;
+  NO.tab = c->d_tab;
+  NO.centres = c->d_centres;
+  NO.radii = c->d_radii;
+  NO.rec = c->d_rec;
+  NO.qn3 = nullptr;
+  NO.coef = c->d_ncoef;
+  NO.tx = tg;
+  NO.tn = tn;
+  NO.u = t;
+  NO.pres = nullptr;
+  const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  k_near_off_K<<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
+  prof_end(c, s, &ev);
+  return launch_check(c, "k_near_off_K");
+}
+
 // ================================================================ ABI
 extern "C" {
 
@@ -582,6 +683,10 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
                                                 NbodySmem<kTS, kNST, true>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_K, NBODY_K, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_offK, NBODY_OFFK, kTPB,
+                                                NbodySmem<kTS, kNST, true>::kBytes);
+  cudaFuncSetAttribute(k_near_off_K, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(near_off_smem_doubles(p) * sizeof(double)));
   e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -744,6 +849,23 @@ int bie_eval_offsurface(bie_ctx* c, const double* f, const double* q, const doub
       overlaps(p, m, u, 3 * m))
     return fail(c, BIE_ERR_ARG, "an output overlaps an input or the other output%s");
   return run_offsurface(c, f, q, tg, m, u, p, (cudaStream_t)s);
+}
+
+int bie_eval_traction(bie_ctx* c, const double* sigma, const double* tg, const double* tn,
+                      int64_t m, double* t, bie_stream_t s) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (m < 0) return fail(c, BIE_ERR_ARG, "m < 0%s");
+  if (m == 0) return BIE_OK;
+  if (!sigma || !tg || !tn || !t)
+    return fail(c, BIE_ERR_ARG, "sigma, targets, normals and t must be non-NULL%s");
+  if (!is_device_ptr(sigma) || !is_device_ptr(tg) || !is_device_ptr(tn) || !is_device_ptr(t))
+    return fail(c, BIE_ERR_ARG, "a buffer is not a device pointer%s");
+  if (overlaps(t, 3 * m, sigma, 3 * c->N) || overlaps(t, 3 * m, tg, 3 * m) ||
+      overlaps(t, 3 * m, tn, 3 * m))
+    return fail(c, BIE_ERR_ARG, "output t overlaps an input%s");
+  return run_traction(c, sigma, tg, tn, m, t, (cudaStream_t)s);
 }
 
 static int stage(bie_ctx* c, double** d, size_t n) {

@@ -34,6 +34,7 @@ struct NbodyArgs {
   int n_chunks;         // source chunks
   int tiles_per_chunk;  // source tiles per chunk
   double pscale;        // 2 mu (pressure)
+  const double* tn = nullptr;  // [M][3] target normals (off-surface traction, OFF && MODE 1)
 };
 
 template <int TS, int NST, bool OFF>
@@ -96,7 +97,8 @@ __device__ __forceinline__ void pair_K(const double2 s0, const double2 s1, const
   acc[2] = fma(dz, sm, acc[2]);
 }
 
-// MODE 0: S + D (rows a3, a7); MODE 1: traction operator K (apply only).
+// MODE 0: S + D (rows a3, a7); MODE 1: traction operator K (apply, or off-surface
+// targets with normals A.tn when OFF).
 template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0>
 __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   using SM = NbodySmem<TS, NST, OFF>;
@@ -125,6 +127,11 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
       xt[r][1] = A.tx[3 * ic + 1];
       xt[r][2] = A.tx[3 * ic + 2];
       lo[r] = 0;
+      if (MODE == 1) {
+        nx[MODE == 1 ? r : 0][0] = A.tn[3 * ic];
+        nx[MODE == 1 ? r : 0][1] = A.tn[3 * ic + 1];
+        nx[MODE == 1 ? r : 0][2] = A.tn[3 * ic + 2];
+      }
     } else {
       xt[r][0] = A.rec[ic * kRec];
       xt[r][1] = A.rec[ic * kRec + 1];
@@ -151,10 +158,10 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
     const int cnt = (int)min((int64_t)TS, A.N - k0);
     unsigned char* base = smraw + st * SM::kStageBytes;
     uint32_t bytes = cnt * kRec * 8;
-    uint32_t qbytes = OFF ? ((cnt + 1) & ~1) * 8 : 0;
+    uint32_t qbytes = (OFF && MODE == 0) ? ((cnt + 1) & ~1) * 8 : 0;
     mbar_arrive_expect_tx(&bar[st], bytes + qbytes);
     bulk_g2s(base, A.rec + k0 * kRec, bytes, &bar[st]);
-    if (OFF) bulk_g2s(base + SM::kRecBytes, A.qn3 + k0, qbytes, &bar[st]);
+    if (OFF && MODE == 0) bulk_g2s(base + SM::kRecBytes, A.qn3 + k0, qbytes, &bar[st]);
   };
 
   if (threadIdx.x == 0) {
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
       for (int sidx = 0; sidx < cnt; ++sidx) {
         const double2* sr = srec + sidx * (kRec / 2);
         const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
-        const double qn = OFF ? sqn[sidx] : 0.0;
+        const double qn = (OFF && MODE == 0) ? sqn[sidx] : 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (MODE == 1)

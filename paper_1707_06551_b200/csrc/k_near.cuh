@@ -286,6 +286,7 @@ struct NearOffArgs {
   const double* tx;    // [M][3]
   double* u;           // [M][3] accumulated
   double* pres;        // [M] accumulated, nullable
+  const double* tn = nullptr;  // [M][3] target normals (traction, k_near_off_K)
 };
 
 __host__ __device__ inline int64_t near_off_smem_doubles(int p) {

@@ -255,4 +255,70 @@ __global__ void __launch_bounds__(128) k_near_K(const NearArgs A) {
   for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
 }
 
+// Off-surface traction targets (bie_eval_traction): one thread per target, the
+// near spheres (0 <= |x - c_s| - a_s < eta 2 a_s, exterior only) found by the
+// same ascending shared-memory scan as k_near_off; t[i] += T_s(x; n) - smooth_K_s.
+__global__ void __launch_bounds__(128) k_near_off_K(const NearOffArgs A) {
+  extern __shared__ __align__(16) double sm[];
+  const int p = A.p, nsn = A.nsn;
+  const TableLayout L(p);
+  const int nlm = L.nlm;
+  double* rt = sm;              // rA, rB, rC
+  double* tile = sm + 3 * nlm;  // [kSphTile][4]
+  for (int e = threadIdx.x; e < 3 * nlm; e += blockDim.x) rt[e] = A.tab[L.rA + e];
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = t < A.M;
+  const int64_t tc = live ? t : A.M - 1;
+  const double x[3] = {A.tx[3 * tc], A.tx[3 * tc + 1], A.tx[3 * tc + 2]};
+  const double nv[3] = {A.tn[3 * tc], A.tn[3 * tc + 1], A.tn[3 * tc + 2]};
+  double du[3] = {0.0, 0.0, 0.0};
+  int list[kNearList];
+  int cnt = 0;
+  auto flush = [&]() {
+    for (int j = 0; j < cnt; ++j) {
+      const int s = list[j];
+      const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+      double ex[3];
+      exterior_traction(p, A.coef + (int64_t)s * nlm * 10, rt, rt + nlm, cs, A.radii[s], x, nv, ex);
+      double acc[3] = {0.0, 0.0, 0.0};
+      const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
+      for (int k = 0; k < nsn; ++k) {
+        const double2* q2 = sr + k * (kRec / 2);
+        pair_K<false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 4), __ldg(q2 + 5), x, nv, acc, 0, 0, 1);
+      }
+      du[0] += ex[0] - acc[0];
+      du[1] += ex[1] - acc[1];
+      du[2] += ex[2] - acc[2];
+    }
+    cnt = 0;
+  };
+  for (int64_t s0 = 0; s0 < A.ns; s0 += kSphTile) {
+    const int nt = (int)min((int64_t)kSphTile, A.ns - s0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt; e += blockDim.x) {
+      tile[4 * e] = A.centres[3 * (s0 + e)];
+      tile[4 * e + 1] = A.centres[3 * (s0 + e) + 1];
+      tile[4 * e + 2] = A.centres[3 * (s0 + e) + 2];
+      tile[4 * e + 3] = A.radii[s0 + e];
+    }
+    __syncthreads();
+    for (int e = 0; e < nt; ++e) {
+      const double dx = __dsub_rn(x[0], tile[4 * e]), dy = __dsub_rn(x[1], tile[4 * e + 1]),
+                   dz = __dsub_rn(x[2], tile[4 * e + 2]);
+      const double a = tile[4 * e + 3];
+      const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+      const double dsurf = __dsub_rn(r, a);
+      if (live && dsurf >= 0.0 && dsurf < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {
+        list[cnt++] = (int)(s0 + e);
+        if (cnt == kNearList) flush();
+      }
+    }
+  }
+  flush();
+  if (!live) return;
+  A.u[3 * t] += du[0];
+  A.u[3 * t + 1] += du[1];
+  A.u[3 * t + 2] += du[2];
+}
+
 }  // namespace bie

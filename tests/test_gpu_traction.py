@@ -152,3 +152,99 @@ def test_K_near_two_spheres_vs_converged_quadrature(bie, oracle_mod, direction):
     ref = (oracle_mod.self_term(c, a, p, 1.0, None, sig, np.arange(nsn)) +
            oracle_mod.K_at(c[1:], a[1:], 96, sigf, x[:nsn], nrm[:nsn]))
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+# --------------------------------------- off-surface traction (bie_eval_traction)
+def gpu_traction(bie, c, a, p, mu, sigma, tg, tn, eta=0.0, chunks=0):
+    ctx = bie.bie_create(c, a, p, mu)
+    if eta > 0:
+        bie.bie_set_near(ctx, eta)
+    if chunks:
+        bie.bie_set_source_chunks(ctx, chunks)
+    t = torch.full((len(tg), 3), np.nan, dtype=torch.float64, device="cuda")
+    bie.bie_eval_traction(ctx, _dev(sigma), _dev(tg), _dev(tn), t)
+    torch.cuda.synchronize()
+    ctx.close()
+    return t.cpu().numpy()
+
+
+def _targets_around(seed, c, a, m):
+    """Targets near surfaces (gaps 0.01a..1a), inside spheres, and in the bulk."""
+    rng = np.random.default_rng(seed)
+    s = rng.integers(0, len(a), m)
+    d = rng.standard_normal((m, 3))
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    rr = np.where(rng.uniform(size=m) < 0.15, rng.uniform(0.2, 0.9, m), 1.0 + rng.uniform(0.01, 1.0, m))
+    tg = c[s] + (a[s] * rr)[:, None] * d
+    nv = rng.standard_normal((m, 3))
+    return tg, nv / np.linalg.norm(nv, axis=1)[:, None]
+
+
+@pytest.mark.parametrize("p,ns,eta,chunks", [(4, 5, 0.0, 0), (6, 7, 1.0, 0), (8, 4, 2.0, 3), (12, 3, 1.0, 0)])
+def test_traction_offsurface_matches_oracle(bie, oracle_mod, p, ns, eta, chunks):
+    c, a, f, _, mu = _random_case(1300 + p, ns, p, True, 1.1)
+    tg, nv = _targets_around(p, c, a, 700)
+    got = gpu_traction(bie, c, a, p, mu, f, tg, nv, eta, chunks)
+    ref = oracle_mod.traction_offsurface(c, a, p, f, tg, nv, eta)
+    _assert_parity(got, ref, f"traction p={p} eta={eta}")
+
+
+def test_traction_offsurface_closed_forms_on_gpu(bie, oracle_mod):
+    """eqs 3.19-3.21 (exterior) at 1.01a..1.8a from one sphere, normal e_r,
+    with the near correction: the device reproduces the closed forms to 1e-12.
+    Target 0 sits on the source's polar axis, where the closed forms' scipy
+    harmonics divide by sin(theta): it is checked against converged
+    fine-grid (p = 64) quadrature of the K kernel instead."""
+    from tests import _harmonics as H
+    from tests.test_oracle_traction import _K_closed_form
+    p, a = 8, 1.4
+    c = np.array([[0.3, -0.2, 0.5]])
+    ctx = bie.bie_create(c, np.array([a]), p, 1.0)
+    N = bie.bie_num_nodes(ctx)
+    x = torch.empty((N, 3), dtype=torch.float64, device="cuda")
+    bie.bie_get_nodes(ctx, x, None, None)
+    xs = x.cpu().numpy()
+    ctx.close()
+    rng = np.random.default_rng(15)
+    th, ph = rng.uniform(0.05, 3.1, 40), rng.uniform(-3.1, 3.1, 40)
+    th[0], ph[0] = 0.0, 0.0  # a target on the source's polar axis
+    er = np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)], 1)
+    rr = rng.uniform(1.01, 1.8, 40)
+    rr[0] = 1.6
+    pts = c[0] + a * rr[:, None] * er
+    xf, _, _ = oracle_mod.nodes(c, np.array([a]), 64)
+    for n, m, ch in ((1, 1, 0), (2, 0, 1), (4, -3, 2), (7, 5, 1), (8, 2, 0)):
+        sig = H.vsh_density(n, m, ch, xs, c[0], a)
+        got = gpu_traction(bie, c, np.array([a]), p, 1.0, sig, pts, er, eta=1.0)
+        ref = np.array([_K_closed_form(n, m, ch, rr[i], th[i], ph[i]) for i in range(1, 40)])
+        assert np.abs(got[1:] - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (n, m, ch)
+        sigf = np.nan_to_num(H.vsh_density(n, m, ch, xf, c[0], a))  # no fine node on the axis
+        pole = oracle_mod.K_at(c, np.array([a]), 64, sigf, pts[:1], er[:1])
+        assert np.abs(got[0] - pole[0]).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (n, m, ch)
+
+
+def test_traction_offsurface_batches_and_edge_cases(bie, oracle_mod):
+    """m = 2^21 + 5 targets spans two internal batches; m = 0 is a no-op;
+    NULL normals are rejected."""
+    p = 4
+    c = np.array([[0.0, 0.0, 0.0], [3.0, 0.0, 0.0]])
+    a = np.ones(2)
+    N = 2 * (p + 1) * (2 * p + 2)
+    sig = np.random.default_rng(16).standard_normal((N, 3))
+    m = (1 << 21) + 5
+    g = torch.Generator(device="cuda").manual_seed(0)
+    tg = torch.rand((m, 3), generator=g, dtype=torch.float64, device="cuda") * 20.0 + 5.0
+    nv = torch.nn.functional.normalize(torch.randn((m, 3), generator=g, dtype=torch.float64, device="cuda"), dim=1)
+    ctx = bie.bie_create(c, a, p, 1.0)
+    t = torch.empty_like(tg)
+    bie.bie_eval_traction(ctx, _dev(sig), tg, nv, t)
+    torch.cuda.synchronize()
+    sel = np.r_[0:3, (1 << 21) - 2:(1 << 21) + 5]
+    ref = oracle_mod.K_at(c, a, p, sig, tg[sel].cpu().numpy(), nv[sel].cpu().numpy())
+    _assert_parity(t[sel].cpu().numpy(), ref, "batched traction")
+    empty = torch.empty((0, 3), dtype=torch.float64, device="cuda")
+    bie.bie_eval_traction(ctx, _dev(sig), empty, empty, empty)
+    with pytest.raises(bie.BieError):
+        bie._abi._check(ctx, bie._abi._lib.bie_eval_traction(ctx.handle, bie._abi._ptr(_dev(sig), device=True),
+                                                             tg.data_ptr(), None, m, t.data_ptr(), None))
+    ctx.close()

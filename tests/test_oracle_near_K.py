@@ -116,3 +116,25 @@ def test_near_K_two_spheres_reproduces_converged_integral(oracle_mod):
     assert np.abs(corr - ref).max() <= 1e-12 * scale
     # eta too small to flag the pair: no correction
     assert np.abs(oracle_mod.near_K(c, a, p, sig, 0.1, sub)).max() == 0.0
+
+
+def test_traction_offsurface_near_surface_closed_forms(oracle_mod):
+    """Off-surface traction evaluator with the near correction: one sphere of
+    radius 1.4 (scaled eqs 3.19-3.21: K is a-free, r -> |x - c|/a), targets at
+    1.01 a .. 1.8 a with normal e_r, where the smooth rule alone is far off;
+    with eta = 1 every target is corrected and the closed forms hold to 1e-12."""
+    p, a = 6, 1.4
+    c = np.array([0.3, -0.2, 0.5])
+    x, _, _ = oracle_mod.nodes(c[None], np.array([a]), p)
+    rng = np.random.default_rng(14)
+    th, ph = rng.uniform(0.1, 3.0, 8), rng.uniform(-3.1, 3.1, 8)
+    er = np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)], 1)
+    rr = np.array([1.01, 1.03, 1.1, 1.2, 1.35, 1.5, 1.65, 1.8])
+    pts = c + a * rr[:, None] * er
+    for n, m, ch in ((1, 0, 0), (2, 1, 1), (3, -2, 2), (5, 4, 1), (6, 3, 0)):
+        sig = H.vsh_density(n, m, ch, x, c, a)
+        t = oracle_mod.traction_offsurface(c[None], np.array([a]), p, sig, pts, er, eta=1.0)
+        t0 = oracle_mod.traction_offsurface(c[None], np.array([a]), p, sig, pts, er, eta=0.0)
+        ref = np.array([_K_closed_form(n, m, ch, rr[i], th[i], ph[i]) for i in range(8)])
+        assert np.abs(t - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (n, m, ch)
+        assert np.abs(t0 - ref).max() >= 1e-6  # the smooth rule alone is not accurate here
