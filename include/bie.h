@@ -251,7 +251,11 @@ int64_t bie_near_pairs(const bie_ctx* ctx);
  *   max_iter operator applications; *iters gets the count, *rel_resid the TRUE
  *   relative residual of the returned mu (recomputed).  Not converging is
  *   not an error (check *rel_resid).  Synchronous; workspace
- *   (restart + 2) x 3N doubles is allocated per call.
+ *   (restart + 2) x 3N doubles is allocated per call.  1 <= restart <= 500;
+ *   restarting costs iterations (cfg 3: restart 30/50/100 -> 114/94/80
+ *   iterations; cfg 5: 50 -> 200, 300 -> 138), so a restart at least as
+ *   long as the expected iteration count is the better use of HBM
+ *   (cfg 5: 300 vectors = 7 GB).
  *   The force on sphere s is -sum_{k in s} w_k mu_k (Stokes drag; pinned in
  *   tests/test_oracle_porous.py).
  *   precond = 1: right preconditioning by the exact inverse of each sphere's

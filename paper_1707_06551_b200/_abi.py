@@ -280,7 +280,7 @@ def bie_near_pairs(ctx) -> int:
     return int(_lib.bie_near_pairs(ctx.handle))
 
 
-def bie_solve_porous(ctx, uinf, mu, tol=1e-12, max_iter=200, restart=50, precond=True, stream=None):
+def bie_solve_porous(ctx, uinf, mu, tol=1e-12, max_iter=400, restart=200, precond=True, stream=None):
     """GMRES solve of BIE 5.4; returns (iterations, true relative residual)."""
     N = bie_num_nodes(ctx)
     it, res = ctypes.c_int(), ctypes.c_double()

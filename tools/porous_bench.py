@@ -30,12 +30,16 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pc = os.environ.get("PRECOND", "1") == "1"
-        it, res = bie.bie_solve_porous(ctx, uinf, mu, tol=1e-10, max_iter=200, restart=50, precond=pc)
+        restart = int(os.environ.get("RESTART", "50"))
+        max_iter = int(os.environ.get("MAX_ITER", "200"))
+        it, res = bie.bie_solve_porous(ctx, uinf, mu, tol=1e-10, max_iter=max_iter, restart=restart,
+                                       precond=pc)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         prof = bie.bie_get_profile(ctx)
         dev_ms = sum(v[0] for v in prof.values())
-        print(json.dumps({"config": cfg, "precond": pc, "n_nodes": N, "iterations": it, "rel_resid": res,
+        print(json.dumps({"config": cfg, "precond": pc, "restart": restart, "max_iter": max_iter,
+                          "n_nodes": N, "iterations": it, "rel_resid": res,
                           "wall_s": wall, "device_ms": dev_ms,
                           "krylov_ms": prof["krylov"][0], "nbody_ms": prof["nbody"][0],
                           "near_ms": prof["near"][0], "self_ms": prof["self"][0],
