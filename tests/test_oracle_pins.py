@@ -495,3 +495,45 @@ def test_self_operator_structure_on_white_noise(oracle_mod, p):
     assert np.sum(sv > 1e-10 * sv[0]) == 3 * (p + 1) ** 2 - 2
     sv = np.linalg.svd(MS, compute_uv=False)
     assert np.sum(sv > 1e-10 * sv[0]) == 3 * (p + 1) ** 2 - 3   # lamS_V(0) = 0
+
+
+@pytest.mark.parametrize("p", [3, 5])
+def test_self_term_on_white_noise_is_the_operator_on_the_R9_interpolant(oracle_mod, p):
+    """Value pin for non-band-limited input.  R9 defines the forward transform
+    as the discrete quadrature projection onto VSH of degree <= p; the self term
+    must then be the CONTINUOUS on-surface S / D_pv (brute-force polar
+    quadrature, independent of the oracle) applied to that band-limited
+    interpolant.  The interpolant is built here from scipy's harmonics."""
+    from tests import _harmonics as H
+    rng = np.random.default_rng(40 + p)
+    a, mu = 1.3, 0.8
+    c = np.array([0.2, -0.1, 0.4])
+    x, _, w = oracle_mod.nodes(c[None], np.array([a]), p)
+    wh = w / a ** 2                       # unit-sphere weights (R4)
+    g = rng.standard_normal(x.shape)      # white noise at the nodes
+    th, ph = H.angles((x - c) / a)
+    modes = []
+    for n in range(p + 1):
+        for m in range(-n, n + 1):
+            Z = H.vsh(n, m, th, ph)
+            for ch in range(3):
+                if n == 0 and ch:
+                    continue
+                norm2 = np.sum(wh[:, None] * np.abs(Z[ch]) ** 2)
+                alpha = np.sum(wh[:, None] * g * np.conj(Z[ch])) / norm2
+                modes.append((n, m, ch, alpha))
+
+    def interp(y):
+        t2, p2 = H.angles((y - c) / a)
+        out = np.zeros(y.shape, dtype=complex)
+        for n, m, ch, al in modes:
+            out += al * H.vsh(n, m, t2, p2)[ch]
+        return np.real(out)
+
+    uS = oracle_mod.self_term(c[None], np.array([a]), p, mu, g, None)
+    uD = oracle_mod.self_term(c[None], np.array([a]), p, mu, None, g)
+    for i in (0, 7, len(x) // 2, len(x) - 1):
+        refS = H.onsurface_layers(x[i], c, a, mu, interp, "S")
+        refD = H.onsurface_layers(x[i], c, a, mu, interp, "D")
+        assert np.abs(uS[i] - refS).max() <= 1e-11 * np.abs(refS).max(), i
+        assert np.abs(uD[i] - refD).max() <= 1e-11 * np.abs(refD).max(), i
