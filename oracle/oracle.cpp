@@ -30,6 +30,13 @@
 //   O-7 oracle_self_addthm  the same self operator built from the addition
 //                           theorem, an internal cross-check
 //   helpers for pins: oracle_ylm, oracle_vsh, oracle_eigen
+// Beyond §8(a), each pinned in tests/test_oracle_*.py:
+//   NEXT-1  oracle_exterior_eval, oracle_is_near, oracle_near,
+//           oracle_exterior_pressure, oracle_near_offsurface
+//   NEXT-3  oracle_far_K, oracle_K_at (eq 2.22, reading R21),
+//           oracle_exterior_traction, oracle_near_K, oracle_near_K_offsurface
+//           (eqs 3.17-3.18, reading R24), oracle_completion (eq 5.8, R22)
+//   (NEXT-2's dense operator and LU solve are in oracle/__init__.py.)
 // =============================================================================
 #include <algorithm>
 #include <cmath>

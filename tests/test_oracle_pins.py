@@ -220,7 +220,8 @@ def test_self_operator_trace(oracle_mod, p):
 @pytest.mark.parametrize("p", [4, 8])
 def test_self_projection_equals_addition_theorem(oracle_mod, p):
     """O-4 (explicit harmonics) == O-7 (addition theorem) on non-band-limited
-    white noise: internal consistency only (parity unpinned by the paper, R9)."""
+    white noise: an internal cross-check (the value pin for white noise is
+    test_self_term_on_white_noise_is_the_operator_on_the_R9_interpolant)."""
     rng = np.random.default_rng(p)
     ns = (p + 1) * (2 * p + 2)
     f, q = rng.standard_normal((ns, 3)), rng.standard_normal((ns, 3))
