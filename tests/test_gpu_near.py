@@ -168,3 +168,19 @@ def test_offsurface_near_config5_subset(bie, oracle_mod):
                                             d["targets"][tsub])
     _assert_parity(u.cpu().numpy()[tsub], uref, "cfg5 near u")
     _assert_parity(pr.cpu().numpy()[tsub], pref, "cfg5 near p")
+
+
+@pytest.mark.parametrize("p", [24, 30])
+def test_near_high_order_unstaged(bie, oracle_mod, p):
+    """p >= 24: a neighbour's records + coefficients no longer fit the 160 KB
+    staging budget, so k_near reads them from global memory (the STAGE = false
+    instantiation).  Three spheres, sampled target nodes."""
+    c = np.array([[0.0, 0.0, 0.0], [2.4, 0.3, -0.2], [-0.5, 2.3, 0.4]])
+    a = np.array([1.0, 0.9, 1.1])
+    N = 3 * (p + 1) * (2 * p + 2)
+    rng = np.random.default_rng(p)
+    f, q = rng.standard_normal((N, 3)), rng.standard_normal((N, 3))
+    got, npairs = gpu_apply_near(bie, c, a, p, 1.2, f, q, 1.0)
+    assert npairs == _count_pairs(oracle_mod, c, a, 1.0) > 0
+    sub = np.arange(0, N, 37)
+    _assert_parity(got[sub], oracle_mod.apply_near(c, a, p, 1.2, f, q, 1.0, sub), f"near p={p}")

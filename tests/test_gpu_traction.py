@@ -248,3 +248,15 @@ def test_traction_offsurface_batches_and_edge_cases(bie, oracle_mod):
         bie._abi._check(ctx, bie._abi._lib.bie_eval_traction(ctx.handle, bie._abi._ptr(_dev(sig), device=True),
                                                              tg.data_ptr(), None, m, t.data_ptr(), None))
     ctx.close()
+
+
+def test_K_near_high_order_unstaged(bie, oracle_mod):
+    """p = 24: k_near_K's unstaged (global-memory) instantiation; sampled nodes."""
+    p = 24
+    c = np.array([[0.0, 0.0, 0.0], [2.4, 0.3, -0.2], [-0.5, 2.3, 0.4]])
+    a = np.array([1.0, 0.9, 1.1])
+    N = 3 * (p + 1) * (2 * p + 2)
+    sig = np.random.default_rng(24).standard_normal((N, 3))
+    got = gpu_K_near(bie, c, a, p, 1.0, sig, 1.0)
+    sub = np.arange(0, N, 37)
+    _assert_parity(got[sub], oracle_mod.apply_K_near(c, a, p, sig, 1.0, sub), "K near p=24")
