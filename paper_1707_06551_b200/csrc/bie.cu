@@ -16,7 +16,6 @@
 #include "k_krylov.cuh"
 #include "k_nbody.cuh"
 #include "k_near.cuh"
-#include "k_near_K.cuh"
 #include "k_self.cuh"
 #include "k_setup.cuh"
 
@@ -311,8 +310,8 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   prof_begin(c, BIE_KIND_NEAR, s, &ev);
   const bool stage = near_stage(c->p);
   const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
-  if (stage) k_near<true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
-  else k_near<false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+  if (stage) k_near<true, false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+  else k_near<false, false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
   prof_end(c, s, &ev);
   return launch_check(c, "k_near");
 }
@@ -456,8 +455,8 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   NO.pres = p;
   const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
   prof_begin(c, BIE_KIND_NEAR, s, &ev);
-  if (p) k_near_off<true><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
-  else k_near_off<false><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
+  if (p) k_near_off<true, false><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
+  else k_near_off<false, false><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
   prof_end(c, s, &ev);
   return launch_check(c, "k_near_off");
 }
@@ -557,9 +556,9 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
   NO.pres = nullptr;
   const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
   prof_begin(c, BIE_KIND_NEAR, s, &ev);
-  k_near_off_K<<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
+  k_near_off<false, true><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
   prof_end(c, s, &ev);
-  return launch_check(c, "k_near_off_K");
+  return launch_check(c, "k_near_off<K>");
 }
 
 // ================================================================ ABI
@@ -665,17 +664,17 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   c->launches[BIE_KIND_SETUP] += 2;
   prof_end(c, 0, &ev);
   set_self_smem(p);
-  cudaFuncSetAttribute(k_near<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p, true) * sizeof(double)));
-  cudaFuncSetAttribute(k_near<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p, false) * sizeof(double)));
-  cudaFuncSetAttribute(k_near_K<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p, true) * sizeof(double)));
-  cudaFuncSetAttribute(k_near_K<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_smem_doubles(p, false) * sizeof(double)));
-  cudaFuncSetAttribute(k_near_off<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near_off<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_off_smem_doubles(p) * sizeof(double)));
-  cudaFuncSetAttribute(k_near_off<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near_off<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_off_smem_doubles(p) * sizeof(double)));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
@@ -685,7 +684,7 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_offK, NBODY_OFFK, kTPB,
                                                 NbodySmem<kTS, kNST, true>::kBytes);
-  cudaFuncSetAttribute(k_near_off_K, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_near_off<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(near_off_smem_doubles(p) * sizeof(double)));
   e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -797,10 +796,10 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
       prof_begin(c, BIE_KIND_NEAR, s, &ev);
       const bool stage = near_stage(c->p);
       const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
-      if (stage) k_near_K<true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
-      else k_near_K<false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+      if (stage) k_near<true, true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
+      else k_near<false, true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
       prof_end(c, s, &ev);
-      rc = launch_check(c, "k_near_K");
+      rc = launch_check(c, "k_near<K>");
       if (rc) return rc;
     }
   }

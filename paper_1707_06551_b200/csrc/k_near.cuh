@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "k_nbody.cuh"
 #include "k_setup.cuh"
+#include "k_traction.cuh"
 
 namespace bie {
 
@@ -77,7 +78,9 @@ __device__ __forceinline__ void exterior_field(int p, const double* __restrict__
 // ascending index) every thread adds exterior_s(x) - smooth_s(x) at its nodes.
 // STAGE: s's packed records and expansion coefficients are copied to shared
 // memory first (broadcast reads in the O(n_s^2) smooth-rule subtraction).
-template <bool STAGE>
+// K = false: velocity of S + D (NEXT-1); K = true: traction of S with the
+// target normal (NEXT-3, exterior_traction and the K pair kernel).
+template <bool STAGE, bool K>
 __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, nsn = A.nsn;
@@ -114,13 +117,23 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
     const double2* sr = reinterpret_cast<const double2*>(rec_s);
     for (int kk = tid; kk < nsn; kk += nt) {
       const int64_t i = (int64_t)t * nsn + kk;
-      const double xt[3] = {A.rec[i * kRec], A.rec[i * kRec + 1], A.rec[i * kRec + 2]};
-      double ex[3];
-      exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
-      double acc[3] = {0.0, 0.0, 0.0}, pdummy = 0.0;
-      for (int k = 0; k < nsn; ++k) {
-        const double2* q2 = sr + k * (kRec / 2);
-        pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
+      const double* ri = A.rec + i * kRec;
+      const double xt[3] = {ri[0], ri[1], ri[2]};
+      double ex[3], acc[3] = {0.0, 0.0, 0.0};
+      if constexpr (K) {
+        const double nx[3] = {ri[3], ri[4], ri[5]};
+        exterior_traction(p, cf, rt, rt + nlm, cs, a, xt, nx, ex);
+        for (int k = 0; k < nsn; ++k) {
+          const double2* q2 = sr + k * (kRec / 2);
+          pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
+        }
+      } else {
+        exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
+        double pdummy = 0.0;
+        for (int k = 0; k < nsn; ++k) {
+          const double2* q2 = sr + k * (kRec / 2);
+          pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
+        }
       }
       du[3 * kk + 0] += ex[0] - acc[0];
       du[3 * kk + 1] += ex[1] - acc[1];
@@ -286,7 +299,7 @@ struct NearOffArgs {
   const double* tx;    // [M][3]
   double* u;           // [M][3] accumulated
   double* pres;        // [M] accumulated, nullable
-  const double* tn = nullptr;  // [M][3] target normals (traction, k_near_off_K)
+  const double* tn = nullptr;  // [M][3] target normals (traction, K = true)
 };
 
 __host__ __device__ inline int64_t near_off_smem_doubles(int p) {
@@ -294,7 +307,8 @@ __host__ __device__ inline int64_t near_off_smem_doubles(int p) {
   return 3LL * nlm + 4LL * kSphTile;
 }
 
-template <bool PRESSURE>
+// K = true: traction with the target normals A.tn (bie_eval_traction, NEXT-3).
+template <bool PRESSURE, bool K>
 __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, nsn = A.nsn;
@@ -307,6 +321,12 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
   const bool live = t < A.M;
   const int64_t tc = live ? t : A.M - 1;
   const double x[3] = {A.tx[3 * tc], A.tx[3 * tc + 1], A.tx[3 * tc + 2]};
+  double nv[3] = {0.0, 0.0, 0.0};
+  if constexpr (K) {
+    nv[0] = A.tn[3 * tc];
+    nv[1] = A.tn[3 * tc + 1];
+    nv[2] = A.tn[3 * tc + 2];
+  }
   double du[3] = {0.0, 0.0, 0.0}, dp = 0.0;
   int list[kNearList];
   int cnt = 0;
@@ -314,17 +334,24 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
     for (int j = 0; j < cnt; ++j) {
       const int s = list[j];
       const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
-      double ex[3], pe = 0.0;
-      exterior_field<PRESSURE>(p, A.coef + (int64_t)s * nlm * 10, rt, rt + nlm, rt + 2 * nlm, cs,
-                               A.radii[s], x, ex, &pe);
-      double acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
+      const double* cf = A.coef + (int64_t)s * nlm * 10;
       const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
-      const double* sq = A.qn3 + (int64_t)s * nsn;
-      for (int k = 0; k < nsn; ++k) {
-        const double2* q2 = sr + k * (kRec / 2);
-        pair_acc<false, PRESSURE>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3),
-                                  __ldg(q2 + 4), __ldg(q2 + 5), PRESSURE ? __ldg(sq + k) : 0.0, x,
-                                  acc, pacc, 0, 0, 1);
+      double ex[3], pe = 0.0, acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
+      if constexpr (K) {
+        exterior_traction(p, cf, rt, rt + nlm, cs, A.radii[s], x, nv, ex);
+        for (int k = 0; k < nsn; ++k) {
+          const double2* q2 = sr + k * (kRec / 2);
+          pair_K<false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 4), __ldg(q2 + 5), x, nv, acc, 0, 0, 1);
+        }
+      } else {
+        exterior_field<PRESSURE>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, A.radii[s], x, ex, &pe);
+        const double* sq = A.qn3 + (int64_t)s * nsn;
+        for (int k = 0; k < nsn; ++k) {
+          const double2* q2 = sr + k * (kRec / 2);
+          pair_acc<false, PRESSURE>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3),
+                                    __ldg(q2 + 4), __ldg(q2 + 5), PRESSURE ? __ldg(sq + k) : 0.0, x,
+                                    acc, pacc, 0, 0, 1);
+        }
       }
       du[0] += ex[0] - acc[0];
       du[1] += ex[1] - acc[1];

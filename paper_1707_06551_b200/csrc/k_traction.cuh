@@ -1,4 +1,5 @@
-// k_near_K.cuh -- near-singular correction of the traction operator K
+// k_traction.cuh -- exact traction of one sphere's single-layer expansion,
+// used by the near-singular correction of the traction operator K
 // (PAPER eqs 3.17-3.18, with the eq 4.5
 // partition of NEXT-1).  For a target node x (normal n) on sphere t and a
 // near source sphere s, the smooth-rule K sum over s's nodes is replaced by
@@ -20,8 +21,6 @@
 // so targets on the source's polar axis are exact.
 #pragma once
 #include "common.cuh"
-#include "k_nbody.cuh"
-#include "k_near.cuh"
 #include "k_setup.cuh"
 
 namespace bie {
@@ -195,130 +194,6 @@ __global__ void k_near_coef_K(int p, int64_t ns, const double* __restrict__ alph
     o[6 + ri] = fX * kS;
     o[8 + ri] = n * fW;
   }
-}
-
-// One CTA per target sphere with near neighbours (as k_near): every thread
-// adds T_s(x; n) - smooth_K_s(x; n) at its nodes, neighbours in ascending index.
-template <bool STAGE>
-__global__ void __launch_bounds__(128) k_near_K(const NearArgs A) {
-  extern __shared__ __align__(16) double sm[];
-  const int p = A.p, nsn = A.nsn;
-  const TableLayout L(p);
-  const int nlm = L.nlm;
-  double* du = sm;
-  double* rt = du + 3 * nsn;
-  double* srec = rt + ((3 * nlm + 1) & ~1);
-  double* scf = srec + 12 * nsn;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int t = A.tgt[blockIdx.x];
-  for (int e = tid; e < 3 * nlm; e += nt) rt[e] = A.tab[L.rA + e];
-  for (int e = tid; e < 3 * nsn; e += nt) du[e] = 0.0;
-  for (int qn = A.nb_off[t]; qn < A.nb_off[t + 1]; ++qn) {
-    const int s = A.nb_idx[qn];
-    const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
-    const double a = A.radii[s];
-    const double* cf = A.coef + (int64_t)s * nlm * 10;
-    const double* rec_s = A.rec + (int64_t)s * nsn * kRec;
-    if (STAGE) {
-      __syncthreads();
-      const double2* g2 = reinterpret_cast<const double2*>(rec_s);
-      double2* s2 = reinterpret_cast<double2*>(srec);
-      for (int e = tid; e < 6 * nsn; e += nt) s2[e] = g2[e];
-      const double2* c2 = reinterpret_cast<const double2*>(cf);
-      double2* d2 = reinterpret_cast<double2*>(scf);
-      for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
-      __syncthreads();
-      cf = scf;
-      rec_s = srec;
-    } else if (qn == A.nb_off[t]) {
-      __syncthreads();
-    }
-    const double2* sr = reinterpret_cast<const double2*>(rec_s);
-    for (int kk = tid; kk < nsn; kk += nt) {
-      const int64_t i = (int64_t)t * nsn + kk;
-      const double* ri = A.rec + i * kRec;
-      const double xt[3] = {ri[0], ri[1], ri[2]};
-      const double nx[3] = {ri[3], ri[4], ri[5]};
-      double ex[3];
-      exterior_traction(p, cf, rt, rt + nlm, cs, a, xt, nx, ex);
-      double acc[3] = {0.0, 0.0, 0.0};
-      for (int k = 0; k < nsn; ++k) {
-        const double2* q2 = sr + k * (kRec / 2);
-        pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
-      }
-      du[3 * kk + 0] += ex[0] - acc[0];
-      du[3 * kk + 1] += ex[1] - acc[1];
-      du[3 * kk + 2] += ex[2] - acc[2];
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
-}
-
-// Off-surface traction targets (bie_eval_traction): one thread per target, the
-// near spheres (0 <= |x - c_s| - a_s < eta 2 a_s, exterior only) found by the
-// same ascending shared-memory scan as k_near_off; t[i] += T_s(x; n) - smooth_K_s.
-__global__ void __launch_bounds__(128) k_near_off_K(const NearOffArgs A) {
-  extern __shared__ __align__(16) double sm[];
-  const int p = A.p, nsn = A.nsn;
-  const TableLayout L(p);
-  const int nlm = L.nlm;
-  double* rt = sm;              // rA, rB, rC
-  double* tile = sm + 3 * nlm;  // [kSphTile][4]
-  for (int e = threadIdx.x; e < 3 * nlm; e += blockDim.x) rt[e] = A.tab[L.rA + e];
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool live = t < A.M;
-  const int64_t tc = live ? t : A.M - 1;
-  const double x[3] = {A.tx[3 * tc], A.tx[3 * tc + 1], A.tx[3 * tc + 2]};
-  const double nv[3] = {A.tn[3 * tc], A.tn[3 * tc + 1], A.tn[3 * tc + 2]};
-  double du[3] = {0.0, 0.0, 0.0};
-  int list[kNearList];
-  int cnt = 0;
-  auto flush = [&]() {
-    for (int j = 0; j < cnt; ++j) {
-      const int s = list[j];
-      const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
-      double ex[3];
-      exterior_traction(p, A.coef + (int64_t)s * nlm * 10, rt, rt + nlm, cs, A.radii[s], x, nv, ex);
-      double acc[3] = {0.0, 0.0, 0.0};
-      const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
-      for (int k = 0; k < nsn; ++k) {
-        const double2* q2 = sr + k * (kRec / 2);
-        pair_K<false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 4), __ldg(q2 + 5), x, nv, acc, 0, 0, 1);
-      }
-      du[0] += ex[0] - acc[0];
-      du[1] += ex[1] - acc[1];
-      du[2] += ex[2] - acc[2];
-    }
-    cnt = 0;
-  };
-  for (int64_t s0 = 0; s0 < A.ns; s0 += kSphTile) {
-    const int nt = (int)min((int64_t)kSphTile, A.ns - s0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nt; e += blockDim.x) {
-      tile[4 * e] = A.centres[3 * (s0 + e)];
-      tile[4 * e + 1] = A.centres[3 * (s0 + e) + 1];
-      tile[4 * e + 2] = A.centres[3 * (s0 + e) + 2];
-      tile[4 * e + 3] = A.radii[s0 + e];
-    }
-    __syncthreads();
-    for (int e = 0; e < nt; ++e) {
-      const double dx = __dsub_rn(x[0], tile[4 * e]), dy = __dsub_rn(x[1], tile[4 * e + 1]),
-                   dz = __dsub_rn(x[2], tile[4 * e + 2]);
-      const double a = tile[4 * e + 3];
-      const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-      const double dsurf = __dsub_rn(r, a);
-      if (live && dsurf >= 0.0 && dsurf < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {
-        list[cnt++] = (int)(s0 + e);
-        if (cnt == kNearList) flush();
-      }
-    }
-  }
-  flush();
-  if (!live) return;
-  A.u[3 * t] += du[0];
-  A.u[3 * t + 1] += du[1];
-  A.u[3 * t + 2] += du[2];
 }
 
 }  // namespace bie

@@ -4,7 +4,7 @@
   --what near   : apply with eta = 1 on cfg 4    (k_near, k_near_coef)
   --what nearoff: off-surface with eta = 1, cfg 5, 200k targets (k_near_off)
   --what self   : self term only, cfg 5          (k_self_t)
-  --what nearK  : K apply with eta = 1 on cfg 4   (k_near_K, k_near_coef_K)"""
+  --what nearK  : K apply with eta = 1 on cfg 4   (k_near<STAGE, K = true>, k_near_coef_K)"""
 import argparse
 import os
 import sys
