@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+python paper_1707_06551_b200/build.py > /dev/null 2>&1
+timeout 1500 python -m pytest tests/test_gpu_fuzz.py -q -m gpu > gpurun_out/r21.log 2>&1
+echo "pytest exit $?"; tail -30 gpurun_out/r21.log
