@@ -249,6 +249,26 @@ static int launch_check(bie_ctx* c, const char* what) {
   return BIE_OK;
 }
 
+// Arguments of the per-sphere self-term kernel (k_self) for this context.
+static SelfArgs self_args(const bie_ctx* c, const double* f, const double* q, double* u, int self,
+                          double* alpha, int precond) {
+  SelfArgs SA;
+  SA.p = c->p;
+  SA.ns = c->ns;
+  SA.mu = c->mu;
+  SA.tab = c->d_tab;
+  SA.centres = c->d_centres;
+  SA.radii = c->d_radii;
+  SA.f = f;
+  SA.q = q;
+  SA.u = u;
+  SA.rec = c->d_rec;
+  SA.self = self;
+  SA.alpha = alpha;
+  SA.precond = precond;
+  return SA;
+}
+
 static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode = 0);
 
 // per-sphere exterior-expansion coefficients from the k_self projections
@@ -263,24 +283,75 @@ static int run_near_coef(bie_ctx* c, cudaStream_t s) {
   return launch_check(c, "k_near_coef");
 }
 
+// Near correction at the nodes (NEXT-1 velocity, K = false; NEXT-3 traction,
+// K = true), after the far field: one CTA per target sphere with neighbours.
+static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K) {
+  NearArgs NA;
+  NA.p = c->p;
+  NA.nsn = c->nsn;
+  NA.tab = c->d_tab;
+  NA.centres = c->d_centres;
+  NA.radii = c->d_radii;
+  NA.rec = c->d_rec;
+  NA.coef = c->d_ncoef;
+  NA.tgt = c->d_near_tgt;
+  NA.nb_off = c->d_nb_off;
+  NA.nb_idx = c->d_nb_idx;
+  NA.u = u;
+  Ev ev;
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  const bool stage = near_stage(c->p);
+  const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
+  const unsigned g = (unsigned)c->n_near_tgt;
+  if (K) {
+    if (stage) k_near<true, true><<<g, 128, nsm, s>>>(NA);
+    else k_near<false, true><<<g, 128, nsm, s>>>(NA);
+  } else {
+    if (stage) k_near<true, false><<<g, 128, nsm, s>>>(NA);
+    else k_near<false, false><<<g, 128, nsm, s>>>(NA);
+  }
+  prof_end(c, s, &ev);
+  return launch_check(c, K ? "k_near<K>" : "k_near");
+}
+
+// Near correction at m arbitrary targets: velocity (+ pressure when p) or,
+// with target normals tn, traction (K).  Accumulates onto u (and p).
+static int run_near_off(bie_ctx* c, const double* tg, const double* tn, int64_t m, double* u,
+                        double* p, cudaStream_t s) {
+  NearOffArgs NO;
+  NO.p = c->p;
+  NO.nsn = c->nsn;
+  NO.ns = c->ns;
+  NO.M = m;
+  NO.mu = c->mu;
+  NO.eta = c->eta;
+  NO.tab = c->d_tab;
+  NO.centres = c->d_centres;
+  NO.radii = c->d_radii;
+  NO.rec = c->d_rec;
+  NO.qn3 = tn ? nullptr : c->d_qn3;
+  NO.coef = c->d_ncoef;
+  NO.tx = tg;
+  NO.tn = tn;
+  NO.u = u;
+  NO.pres = tn ? nullptr : p;
+  const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
+  const unsigned g = (unsigned)((m + 127) / 128);
+  Ev ev;
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  if (tn) k_near_off<false, true><<<g, 128, sm, s>>>(NO);
+  else if (p) k_near_off<true, false><<<g, 128, sm, s>>>(NO);
+  else k_near_off<false, false><<<g, 128, sm, s>>>(NO);
+  prof_end(c, s, &ev);
+  return launch_check(c, tn ? "k_near_off<K>" : "k_near_off");
+}
+
 static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
                      cudaStream_t s) {
   // rows a2 + a4-a6: self term (or zeros) into u, packed sources into d_rec
-  SelfArgs SA;
-  SA.p = c->p;
-  SA.ns = c->ns;
-  SA.mu = c->mu;
-  SA.tab = c->d_tab;
-  SA.centres = c->d_centres;
-  SA.radii = c->d_radii;
-  SA.f = f;
-  SA.q = q;
-  SA.u = u;
-  SA.rec = c->d_rec;
-  SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
   const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
-  SA.alpha = near ? c->d_alpha : nullptr;
-  SA.precond = 0;
+  const SelfArgs SA =
+      self_args(c, f, q, u, (parts & BIE_PART_SELF) ? 1 : 0, near ? c->d_alpha : nullptr, 0);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
   launch_self(SA, s);
@@ -295,25 +366,7 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
   rc = run_far(c, u, s);
   if (rc || !near) return rc;
   // NEXT-1: replace the smooth rule by the exterior expansion for near pairs
-  NearArgs NA;
-  NA.p = c->p;
-  NA.nsn = c->nsn;
-  NA.tab = c->d_tab;
-  NA.centres = c->d_centres;
-  NA.radii = c->d_radii;
-  NA.rec = c->d_rec;
-  NA.coef = c->d_ncoef;
-  NA.tgt = c->d_near_tgt;
-  NA.nb_off = c->d_nb_off;
-  NA.nb_idx = c->d_nb_idx;
-  NA.u = u;
-  prof_begin(c, BIE_KIND_NEAR, s, &ev);
-  const bool stage = near_stage(c->p);
-  const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
-  if (stage) k_near<true, false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
-  else k_near<false, false><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
-  prof_end(c, s, &ev);
-  return launch_check(c, "k_near");
+  return run_near(c, u, s, false);
 }
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
@@ -368,20 +421,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   const bool near = c->eta > 0.0 && c->d_alpha;
   int rc;
   if (near) {  // NEXT-1 at targets: VSH projections of every sphere, then coefficients
-    SelfArgs SA;
-    SA.p = c->p;
-    SA.ns = c->ns;
-    SA.mu = c->mu;
-    SA.tab = c->d_tab;
-    SA.centres = c->d_centres;
-    SA.radii = c->d_radii;
-    SA.f = f;
-    SA.q = q;
-    SA.u = nullptr;
-    SA.rec = c->d_rec;
-    SA.self = 0;
-    SA.alpha = c->d_alpha;
-    SA.precond = 0;
+    const SelfArgs SA = self_args(c, f, q, nullptr, 0, c->d_alpha, 0);
     prof_begin(c, BIE_KIND_SELF, s, &ev);
     launch_self(SA, s);
     prof_end(c, s, &ev);
@@ -437,28 +477,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
     if (rc) return rc;
   }
   if (!near) return BIE_OK;
-  NearOffArgs NO;
-  NO.p = c->p;
-  NO.nsn = c->nsn;
-  NO.ns = c->ns;
-  NO.M = m;
-  NO.mu = c->mu;
-  NO.eta = c->eta;
-  NO.tab = c->d_tab;
-  NO.centres = c->d_centres;
-  NO.radii = c->d_radii;
-  NO.rec = c->d_rec;
-  NO.qn3 = c->d_qn3;
-  NO.coef = c->d_ncoef;
-  NO.tx = tg;
-  NO.u = u;
-  NO.pres = p;
-  const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
-  prof_begin(c, BIE_KIND_NEAR, s, &ev);
-  if (p) k_near_off<true, false><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
-  else k_near_off<false, false><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
-  prof_end(c, s, &ev);
-  return launch_check(c, "k_near_off");
+  return run_near_off(c, tg, nullptr, m, u, p, s);
 }
 
 // NEXT-3 off the surface: traction K[sigma](x; n) at m targets with normals
@@ -468,20 +487,7 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
   int rc;
   const bool near = c->eta > 0.0 && c->d_alpha;
   if (near) {  // projections of sigma (q slot) -> exterior S coefficients
-    SelfArgs SA;
-    SA.p = c->p;
-    SA.ns = c->ns;
-    SA.mu = c->mu;
-    SA.tab = c->d_tab;
-    SA.centres = c->d_centres;
-    SA.radii = c->d_radii;
-    SA.f = nullptr;
-    SA.q = sigma;
-    SA.u = nullptr;
-    SA.rec = c->d_rec;
-    SA.self = 0;
-    SA.alpha = c->d_alpha;
-    SA.precond = 0;
+    const SelfArgs SA = self_args(c, nullptr, sigma, nullptr, 0, c->d_alpha, 0);
     prof_begin(c, BIE_KIND_SELF, s, &ev);
     launch_self(SA, s);
     prof_end(c, s, &ev);
@@ -537,28 +543,7 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
     if ((rc = launch_check(c, "k_reduce"))) return rc;
   }
   if (!near) return BIE_OK;
-  NearOffArgs NO;
-  NO.p = c->p;
-  NO.nsn = c->nsn;
-  NO.ns = c->ns;
-  NO.M = m;
-  NO.mu = c->mu;
-  NO.eta = c->eta;
-  NO.tab = c->d_tab;
-  NO.centres = c->d_centres;
-  NO.radii = c->d_radii;
-  NO.rec = c->d_rec;
-  NO.qn3 = nullptr;
-  NO.coef = c->d_ncoef;
-  NO.tx = tg;
-  NO.tn = tn;
-  NO.u = t;
-  NO.pres = nullptr;
-  const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
-  prof_begin(c, BIE_KIND_NEAR, s, &ev);
-  k_near_off<false, true><<<(unsigned)((m + 127) / 128), 128, sm, s>>>(NO);
-  prof_end(c, s, &ev);
-  return launch_check(c, "k_near_off<K>");
+  return run_near_off(c, tg, tn, m, t, nullptr, s);
 }
 
 // ================================================================ ABI
@@ -747,21 +732,10 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   if (overlaps(u, n3, sigma, n3)) return fail(c, BIE_ERR_ARG, "output u overlaps sigma%s");
   cudaStream_t s = (cudaStream_t)st;
   // self term: K_pv has the D_pv spectrum; packs q' = (3/4pi) w sigma
-  SelfArgs SA;
-  SA.p = c->p;
-  SA.ns = c->ns;
-  SA.mu = c->mu;
-  SA.tab = c->d_tab;
-  SA.centres = c->d_centres;
-  SA.radii = c->d_radii;
-  SA.f = nullptr;
-  SA.q = sigma;
-  SA.u = u;
-  SA.rec = c->d_rec;
-  SA.self = (parts & BIE_PART_SELF) ? 1 : 0;
   const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
-  SA.alpha = near ? c->d_alpha : nullptr;  // projections of sigma (q slot)
-  SA.precond = 0;
+  // projections of sigma land in the q slot of alpha (k_near_coef_K reads them there)
+  const SelfArgs SA = self_args(c, nullptr, sigma, u, (parts & BIE_PART_SELF) ? 1 : 0,
+                                near ? c->d_alpha : nullptr, 0);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
   launch_self(SA, s);
@@ -781,25 +755,7 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
     rc = run_far(c, u, s, 1);
     if (rc) return rc;
     if (near) {  // traction of the exact exterior expansion for near pairs
-      NearArgs NA;
-      NA.p = c->p;
-      NA.nsn = c->nsn;
-      NA.tab = c->d_tab;
-      NA.centres = c->d_centres;
-      NA.radii = c->d_radii;
-      NA.rec = c->d_rec;
-      NA.coef = c->d_ncoef;
-      NA.tgt = c->d_near_tgt;
-      NA.nb_off = c->d_nb_off;
-      NA.nb_idx = c->d_nb_idx;
-      NA.u = u;
-      prof_begin(c, BIE_KIND_NEAR, s, &ev);
-      const bool stage = near_stage(c->p);
-      const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
-      if (stage) k_near<true, true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
-      else k_near<false, true><<<(unsigned)c->n_near_tgt, 128, nsm, s>>>(NA);
-      prof_end(c, s, &ev);
-      rc = launch_check(c, "k_near<K>");
+      rc = run_near(c, u, s, true);
       if (rc) return rc;
     }
   }
@@ -1099,20 +1055,7 @@ struct Krylov {
   }
   // y = P^{-1} x, P = 1/2 I + S_self + D_self (block diagonal, exact via the spectra)
   int prec(const double* x, double* y) {
-    SelfArgs SA;
-    SA.p = c->p;
-    SA.ns = c->ns;
-    SA.mu = c->mu;
-    SA.tab = c->d_tab;
-    SA.centres = c->d_centres;
-    SA.radii = c->d_radii;
-    SA.f = nullptr;
-    SA.q = x;
-    SA.u = y;
-    SA.rec = c->d_rec;
-    SA.self = 1;
-    SA.alpha = nullptr;
-    SA.precond = 1;
+    const SelfArgs SA = self_args(c, nullptr, x, y, 1, nullptr, 1);
     Ev ev;
     prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
     launch_self(SA, s);
