@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   const int64_t cta_lo = (first / A.nsn) * A.nsn;
   const int64_t cta_hi = (last / A.nsn + 1) * A.nsn;
 
+  const uint64_t pol = l2_evict_last_policy();  // records are re-read by every target tile
   auto issue = [&](int it) {
     const int st = it % NST;
     const int64_t k0 = (tile0 + it) * TS;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
     uint32_t bytes = cnt * kRec * 8;
     uint32_t qbytes = (OFF && MODE == 0) ? ((cnt + 1) & ~1) * 8 : 0;
     mbar_arrive_expect_tx(&bar[st], bytes + qbytes);
-    bulk_g2s(base, A.rec + k0 * kRec, bytes, &bar[st]);
+    bulk_g2s_hint(base, A.rec + k0 * kRec, bytes, &bar[st], pol);
     if (OFF && MODE == 0) bulk_g2s(base + SM::kRecBytes, A.qn3 + k0, qbytes, &bar[st]);
   };
 
@@ -233,11 +234,11 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
       if (OFF && A.pout) A.pout[li] = A.pscale * pacc[r];
     } else {
       const int64_t Mb = A.M;
-      double* po = A.uout + ((int64_t)chunk * Mb + li) * 3;
-      po[0] = acc[r][0];
-      po[1] = acc[r][1];
-      po[2] = acc[r][2];
-      if (OFF && A.pout) A.pout[(int64_t)chunk * Mb + li] = pacc[r];
+      double* po = A.uout + ((int64_t)chunk * Mb + li) * 3;  // read once by k_reduce: streaming
+      __stcs(po, acc[r][0]);
+      __stcs(po + 1, acc[r][1]);
+      __stcs(po + 2, acc[r][2]);
+      if (OFF && A.pout) __stcs(A.pout + (int64_t)chunk * Mb + li, pacc[r]);
     }
   }
 }
