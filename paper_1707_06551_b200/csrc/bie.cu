@@ -23,19 +23,21 @@ using namespace bie;
 
 namespace {
 
-// Far-field kernel configuration: R targets per thread,
-// TPB threads, TS sources per shared-memory tile, NST pipeline stages.
-// Chosen by tools/nbody_tune.cu on B200: 8 targets per thread
-// maximises operand reuse of the shared source registers.
-constexpr int kR = 8, kTPB = 64, kTS = 64, kNST = 3;
-constexpr int kTgtTile = kR * kTPB;
+// Far-field kernel configurations: R targets per thread,
+// TPB threads, TS sources per shared-memory tile, NST pipeline stages, source
+// loop unroll.  Chosen per kernel by tools/nbody_tune.cu on B200
+// (profiles/r01_nbody_tune.txt): 8 targets per thread for the SL+DL apply,
+// 7 for the off-surface and traction kernels (their extra per-target
+// registers -- pressure, normals -- make 8 spill-prone and RF-read bound).
+constexpr int kTPB = 64, kTS = 64, kNST = 3;
+constexpr int kR_APPLY = 8, kR_OFF = 7, kR_K = 7, kR_OFFK = 7;
 constexpr int64_t kOffBatch = 1 << 21;  // off-surface targets per batch (bounds scratch)
 constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 
-#define NBODY_APPLY k_nbody<kR, kTPB, kTS, kNST, false, 1, 2>
-#define NBODY_OFF k_nbody<kR, kTPB, kTS, kNST, true, 1, 1>
-#define NBODY_K k_nbody<kR, kTPB, kTS, kNST, false, 1, 2, 1>
-#define NBODY_OFFK k_nbody<kR, kTPB, kTS, kNST, true, 1, 1, 1>
+#define NBODY_APPLY k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2>
+#define NBODY_OFF k_nbody<kR_OFF, kTPB, kTS, kNST, true, 1, 2>
+#define NBODY_K k_nbody<kR_K, kTPB, kTS, kNST, false, 1, 2, 1>
+#define NBODY_OFFK k_nbody<kR_OFFK, kTPB, kTS, kNST, true, 1, 2, 1>
 
 struct Ev {
   int kind;
@@ -188,9 +190,10 @@ struct ChunkPlan {
   int n_tt, n_chunks, tiles_per_chunk;
 };
 
-static ChunkPlan plan_chunks(const bie_ctx* c, int64_t M, int64_t N, int occ) {
+static ChunkPlan plan_chunks(const bie_ctx* c, int64_t M, int64_t N, int occ, int r) {
   ChunkPlan P;
-  P.n_tt = (int)((M + kTgtTile - 1) / kTgtTile);
+  const int64_t tile = (int64_t)r * kTPB;  // targets per CTA
+  P.n_tt = (int)((M + tile - 1) / tile);
   const int64_t n_src_tiles = (N + kTS - 1) / kTS;
   int64_t S;
   if (c->chunks_override > 0) {
@@ -373,7 +376,8 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
 static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode) {
   Ev ev;
   int rc;
-  const ChunkPlan P = plan_chunks(c, c->N, c->N, mode ? c->occ_K : c->occ_apply);
+  const ChunkPlan P =
+      plan_chunks(c, c->N, c->N, mode ? c->occ_K : c->occ_apply, mode ? kR_K : kR_APPLY);
   const int kind = mode ? BIE_KIND_KFAR : BIE_KIND_NBODY;
   NbodyArgs A;
   A.rec = c->d_rec;
@@ -437,7 +441,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
   for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
     const int64_t Mb = std::min(kOffBatch, m - b0);
-    const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_off);
+    const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_off, kR_OFF);
     NbodyArgs A;
     A.rec = c->d_rec;
     A.qn3 = c->d_qn3;
@@ -507,7 +511,7 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
   const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
   for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
     const int64_t Mb = std::min(kOffBatch, m - b0);
-    const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_offK);
+    const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_offK, kR_OFFK);
     NbodyArgs A;
     A.rec = c->d_rec;
     A.qn3 = nullptr;

@@ -11,9 +11,9 @@
 
 using namespace bie;
 
-template <int R, int TPB, int TS, int NST, bool OFF, int MINB, int UNR>
+template <int R, int TPB, int TS, int NST, bool OFF, int MINB, int UNR, int MODE = 0>
 void run(const char* name, const NbodyArgs& base, int sm, double pairs, int reps) {
-  auto kern = k_nbody<R, TPB, TS, NST, OFF, MINB, UNR>;
+  auto kern = k_nbody<R, TPB, TS, NST, OFF, MINB, UNR, MODE>;
   const int smem = NbodySmem<TS, NST, OFF>::kBytes;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, smem);
@@ -30,7 +30,7 @@ void run(const char* name, const NbodyArgs& base, int sm, double pairs, int reps
   double* part;
   cudaMalloc(&part, (size_t)A.n_chunks * 4 * A.M * sizeof(double));
   A.uout = part;
-  A.pout = OFF ? part + (size_t)A.n_chunks * 3 * A.M : nullptr;
+  A.pout = (OFF && MODE == 0) ? part + (size_t)A.n_chunks * 3 * A.M : nullptr;
   A.uinit = nullptr;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -49,7 +49,7 @@ void run(const char* name, const NbodyArgs& base, int sm, double pairs, int reps
     }
   }
   cudaError_t err = cudaGetLastError();
-  const double ops = OFF ? 32.0 : 30.0;
+  const double ops = MODE == 1 ? 25.0 : (OFF ? 32.0 : 30.0);
   const double pps = pairs / (best * 1e-3);
   printf("{\"variant\": \"%s\", \"regs\": %d, \"occ\": %d, \"chunks\": %d, \"ms\": %.3f, \"ms_mean\": %.3f, "
          "\"pairs_per_s\": %.4e, \"pipe_frac_1965\": %.4f, \"err\": \"%s\"}\n",
@@ -68,7 +68,7 @@ int main(int argc, char** argv) {
   cudaGetDeviceProperties(&prop, 0);
   std::mt19937_64 g(7);
   std::uniform_real_distribution<double> U(-1.0, 1.0);
-  std::vector<double> rec(N * kRec + 2 * kRec), qn3(N + 2), tx(3 * N);
+  std::vector<double> rec(N * kRec + 2 * kRec), qn3(N + 2), tx(3 * N), tn(3 * N);
   for (int64_t s = 0; s < ns; ++s) {
     double c[3] = {U(g) * 30, U(g) * 30, U(g) * 30};
     for (int k = 0; k < nsn; ++k) {
@@ -81,11 +81,14 @@ int main(int argc, char** argv) {
         rec[i * kRec + 6 + d] = U(g) * 0.01;
         rec[i * kRec + 9 + d] = U(g) * 0.01;
         tx[3 * i + d] = c[d] + 1.7 * n[d] / r;
+        tn[3 * i + d] = n[d] / r;
       }
       qn3[i] = U(g) * 0.01;
     }
   }
-  double *drec, *dqn, *dtx;
+  double *drec, *dqn, *dtx, *dtn;
+  cudaMalloc(&dtn, tn.size() * 8);
+  cudaMemcpy(dtn, tn.data(), tn.size() * 8, cudaMemcpyHostToDevice);
   cudaMalloc(&drec, rec.size() * 8);
   cudaMalloc(&dqn, qn3.size() * 8);
   cudaMalloc(&dtx, tx.size() * 8);
@@ -96,6 +99,7 @@ int main(int argc, char** argv) {
   A.rec = drec;
   A.qn3 = dqn;
   A.tx = dtx;
+  A.tn = dtn;
   A.N = N;
   A.M = N;
   A.nsn = nsn;
@@ -103,12 +107,38 @@ int main(int argc, char** argv) {
   const double pairs_apply = (double)N * (N - nsn), pairs_off = (double)N * N;
   const int sm = prop.multiProcessorCount;
   printf("# N = %lld, SMs = %d\n", (long long)N, sm);
-  run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 u2 (library)", A, sm, pairs_apply, reps);
-  run<8, 64, 64, 3, true, 1, 1>("off R8 T64 u1 (library)", A, sm, pairs_off, reps);
-  run<8, 64, 64, 3, true, 1, 2>("off R8 T64 u2", A, sm, pairs_off, reps);
-  run<8, 64, 128, 3, true, 1, 1>("off R8 T64 TS128 u1", A, sm, pairs_off, reps);
-  run<8, 32, 64, 3, true, 1, 1>("off R8 T32 u1", A, sm, pairs_off, reps);
-  run<7, 64, 64, 3, true, 1, 1>("off R7 T64 u1", A, sm, pairs_off, reps);
-  run<6, 64, 64, 3, true, 1, 2>("off R6 T64 u2", A, sm, pairs_off, reps);
+  const bool k_only = argc > 3 && argv[3][0] == 'K';  // "K": K variants only; "A": apply/off only
+  if (!k_only) {
+    run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 u2 (library)", A, sm, pairs_apply, reps);
+    run<8, 64, 64, 3, true, 1, 1>("off R8 T64 u1 (library)", A, sm, pairs_off, reps);
+    run<8, 64, 64, 3, true, 1, 2>("off R8 T64 u2", A, sm, pairs_off, reps);
+    run<8, 64, 128, 3, true, 1, 1>("off R8 T64 TS128 u1", A, sm, pairs_off, reps);
+    run<8, 32, 64, 3, true, 1, 1>("off R8 T32 u1", A, sm, pairs_off, reps);
+    run<7, 64, 64, 3, true, 1, 1>("off R7 T64 u1", A, sm, pairs_off, reps);
+    run<6, 64, 64, 3, true, 1, 2>("off R6 T64 u2", A, sm, pairs_off, reps);
+    run<7, 64, 64, 3, false, 1, 2>("apply R7 T64 u2", A, sm, pairs_apply, reps);
+    run<7, 64, 64, 3, false, 1, 1>("apply R7 T64 u1", A, sm, pairs_apply, reps);
+    run<7, 64, 64, 3, false, 1, 4>("apply R7 T64 u4", A, sm, pairs_apply, reps);
+    run<8, 64, 64, 3, false, 1, 4>("apply R8 T64 u4", A, sm, pairs_apply, reps);
+    run<7, 64, 64, 3, true, 1, 2>("off R7 T64 u2", A, sm, pairs_off, reps);
+    run<8, 64, 64, 3, true, 1, 4>("off R8 T64 u4", A, sm, pairs_off, reps);
+  }
+  if (argc > 3 && argv[3][0] == 'A') return 0;
+  // traction operator K (MODE 1): apply (target normals from the records) and off-surface
+  run<8, 64, 64, 3, false, 1, 2, 1>("K apply R8 T64 u2 (library)", A, sm, pairs_apply, reps);
+  run<8, 64, 64, 3, false, 1, 1, 1>("K apply R8 T64 u1", A, sm, pairs_apply, reps);
+  run<8, 64, 64, 3, false, 1, 4, 1>("K apply R8 T64 u4", A, sm, pairs_apply, reps);
+  run<7, 64, 64, 3, false, 1, 1, 1>("K apply R7 T64 u1", A, sm, pairs_apply, reps);
+  run<7, 64, 64, 3, false, 1, 4, 1>("K apply R7 T64 u4", A, sm, pairs_apply, reps);
+  run<7, 64, 64, 3, false, 1, 2, 1>("K apply R7 T64 u2", A, sm, pairs_apply, reps);
+  run<6, 64, 64, 3, false, 1, 2, 1>("K apply R6 T64 u2", A, sm, pairs_apply, reps);
+  run<6, 64, 64, 3, false, 1, 1, 1>("K apply R6 T64 u1", A, sm, pairs_apply, reps);
+  run<4, 128, 64, 3, false, 1, 2, 1>("K apply R4 T128 u2", A, sm, pairs_apply, reps);
+  run<8, 32, 64, 3, false, 1, 2, 1>("K apply R8 T32 u2", A, sm, pairs_apply, reps);
+  run<8, 64, 64, 3, true, 1, 1, 1>("K off R8 T64 u1 (library)", A, sm, pairs_off, reps);
+  run<8, 64, 64, 3, true, 1, 2, 1>("K off R8 T64 u2", A, sm, pairs_off, reps);
+  run<6, 64, 64, 3, true, 1, 2, 1>("K off R6 T64 u2", A, sm, pairs_off, reps);
+  run<7, 64, 64, 3, true, 1, 2, 1>("K off R7 T64 u2", A, sm, pairs_off, reps);
+  run<6, 64, 64, 3, true, 1, 1, 1>("K off R6 T64 u1", A, sm, pairs_off, reps);
   return 0;
 }
