@@ -124,6 +124,22 @@ int main(int argc, char** argv) {
     run<8, 64, 64, 3, true, 1, 4>("off R8 T64 u4", A, sm, pairs_off, reps);
   }
   if (argc > 3 && argv[3][0] == 'A') return 0;
+  if (argc > 3 && argv[3][0] == 'P') {  // apply: pipeline depth / tile size / unroll
+    run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 TS64 NST3 u2 (library)", A, sm, pairs_apply, reps);
+    run<8, 64, 64, 2, false, 1, 2>("apply R8 T64 TS64 NST2 u2", A, sm, pairs_apply, reps);
+    run<8, 64, 64, 4, false, 1, 2>("apply R8 T64 TS64 NST4 u2", A, sm, pairs_apply, reps);
+    run<8, 64, 32, 4, false, 1, 2>("apply R8 T64 TS32 NST4 u2", A, sm, pairs_apply, reps);
+    run<8, 64, 128, 2, false, 1, 2>("apply R8 T64 TS128 NST2 u2", A, sm, pairs_apply, reps);
+    run<8, 64, 128, 3, false, 1, 2>("apply R8 T64 TS128 NST3 u2", A, sm, pairs_apply, reps);
+    run<8, 64, 64, 3, false, 1, 3>("apply R8 T64 TS64 NST3 u3", A, sm, pairs_apply, reps);
+    run<8, 96, 64, 3, false, 1, 2>("apply R8 T96 TS64 NST3 u2", A, sm, pairs_apply, reps);
+    run<8, 128, 64, 3, false, 1, 2>("apply R8 T128 TS64 NST3 u2", A, sm, pairs_apply, reps);
+    run<7, 64, 64, 3, true, 1, 2>("off R7 T64 TS64 NST3 u2 (library)", A, sm, pairs_off, reps);
+    run<7, 64, 64, 4, true, 1, 2>("off R7 T64 TS64 NST4 u2", A, sm, pairs_off, reps);
+    run<7, 64, 128, 3, true, 1, 2>("off R7 T64 TS128 NST3 u2", A, sm, pairs_off, reps);
+    run<7, 64, 64, 3, true, 1, 4>("off R7 T64 TS64 NST3 u4", A, sm, pairs_off, reps);
+    return 0;
+  }
   // traction operator K (MODE 1): apply (target normals from the records) and off-surface
   run<8, 64, 64, 3, false, 1, 2, 1>("K apply R8 T64 u2 (library)", A, sm, pairs_apply, reps);
   run<8, 64, 64, 3, false, 1, 1, 1>("K apply R8 T64 u1", A, sm, pairs_apply, reps);
