@@ -650,21 +650,29 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   k_tables<<<((p + 1) * (p + 1) + 127) / 128, 128>>>(p, c->d_tab);
   k_nodes<<<(unsigned)((c->N + 255) / 256), 256>>>(p, c->N, c->d_tab, c->d_centres, c->d_radii,
                                                   c->d_x, c->d_n, c->d_w);
-  c->launches[BIE_KIND_SETUP] += 2;
+  c->launches[BIE_KIND_SETUP] += 3;
   prof_end(c, 0, &ev);
   set_self_smem(p);
-  cudaFuncSetAttribute(k_near<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_smem_doubles(p, true) * sizeof(double)));
-  cudaFuncSetAttribute(k_near<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_smem_doubles(p, false) * sizeof(double)));
-  cudaFuncSetAttribute(k_near<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_smem_doubles(p, true) * sizeof(double)));
-  cudaFuncSetAttribute(k_near<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_smem_doubles(p, false) * sizeof(double)));
-  cudaFuncSetAttribute(k_near_off<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_off_smem_doubles(p) * sizeof(double)));
-  cudaFuncSetAttribute(k_near_off<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_off_smem_doubles(p) * sizeof(double)));
+  // Dynamic shared memory opt-ins.  A staged near-correction variant whose
+  // footprint exceeds the device limit is never launched (near_stage picks the
+  // unstaged one), so it is skipped rather than requested.
+  const size_t optin = (size_t)prop.sharedMemPerBlockOptin;
+  cudaError_t se = cudaSuccess;
+  auto smem = [&](const void* kern, size_t bytes) {
+    if (bytes <= 48 * 1024 || bytes > optin) return;
+    const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (r != cudaSuccess && se == cudaSuccess) se = r;
+  };
+  const size_t near_st = near_smem_doubles(p, true) * sizeof(double);
+  const size_t near_un = near_smem_doubles(p, false) * sizeof(double);
+  const size_t near_off = near_off_smem_doubles(p) * sizeof(double);
+  smem((const void*)k_near<true, false>, near_st);
+  smem((const void*)k_near<false, false>, near_un);
+  smem((const void*)k_near<true, true>, near_st);
+  smem((const void*)k_near<false, true>, near_un);
+  smem((const void*)k_near_off<true, false>, near_off);
+  smem((const void*)k_near_off<false, false>, near_off);
+  smem((const void*)k_near_off<false, true>, near_off);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
@@ -673,8 +681,11 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_offK, NBODY_OFFK, kTPB,
                                                 NbodySmem<kTS, kNST, true>::kBytes);
-  cudaFuncSetAttribute(k_near_off<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(near_off_smem_doubles(p) * sizeof(double)));
+  if (se != cudaSuccess) {
+    cudaGetLastError();
+    bie_destroy(c);
+    return BIE_ERR_CUDA;
+  }
   e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
