@@ -124,6 +124,15 @@ int main(int argc, char** argv) {
     run<8, 64, 64, 3, true, 1, 4>("off R8 T64 u4", A, sm, pairs_off, reps);
   }
   if (argc > 3 && argv[3][0] == 'A') return 0;
+  if (argc > 3 && argv[3][0] == 'S') {  // small N (cfg 2 size): blocking vs tail/overheads
+    run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 (library)", A, sm, pairs_apply, reps);
+    run<4, 64, 64, 3, false, 1, 2>("apply R4 T64", A, sm, pairs_apply, reps);
+    run<4, 128, 64, 3, false, 1, 2>("apply R4 T128", A, sm, pairs_apply, reps);
+    run<8, 32, 64, 3, false, 1, 2>("apply R8 T32", A, sm, pairs_apply, reps);
+    run<6, 64, 64, 3, false, 1, 2>("apply R6 T64", A, sm, pairs_apply, reps);
+    run<8, 64, 32, 3, false, 1, 2>("apply R8 T64 TS32", A, sm, pairs_apply, reps);
+    return 0;
+  }
   if (argc > 3 && argv[3][0] == 'P') {  // apply: pipeline depth / tile size / unroll
     run<8, 64, 64, 3, false, 1, 2>("apply R8 T64 TS64 NST3 u2 (library)", A, sm, pairs_apply, reps);
     run<8, 64, 64, 2, false, 1, 2>("apply R8 T64 TS64 NST2 u2", A, sm, pairs_apply, reps);
