@@ -260,3 +260,17 @@ def test_K_near_high_order_unstaged(bie, oracle_mod):
     got = gpu_K_near(bie, c, a, p, 1.0, sig, 1.0)
     sub = np.arange(0, N, 37)
     _assert_parity(got[sub], oracle_mod.apply_K_near(c, a, p, sig, 1.0, sub), "K near p=24")
+
+
+def test_half_plus_K_plus_L_on_rigid_density_single_sphere(bie, oracle_mod):
+    """Eq 5.8's left operator on one sphere: (1/2 I + K_pv) annihilates rigid
+    densities (K_pv = D_pv on the sphere, and D_pv[rigid] = -rigid/2),
+    so (1/2 I + K + L)[F + W x (y - c)] = 4 pi a^2 F + (8 pi a^4/3) W x (x - c)."""
+    p, a = 9, 1.3
+    c = np.array([[0.4, -0.2, 0.1]])
+    x, _, _ = oracle_mod.nodes(c, np.array([a]), p)
+    F, W = np.array([0.3, -1.1, 0.6]), np.array([-0.7, 0.2, 0.9])
+    sig = F + np.cross(W, x - c[0])
+    got = 0.5 * sig + gpu_K(bie, c, np.array([a]), p, 1.0, sig, parts=7)
+    ref = 4 * np.pi * a ** 2 * F + (8 * np.pi * a ** 4 / 3) * np.cross(W, x - c[0])
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
