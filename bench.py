@@ -44,6 +44,19 @@ FP64_LANES = 64          # FP64 FMA lanes per SM (B200)
 SM_MAX_MHZ = 1965.0
 
 
+def _hbm_peak_gbps():
+    """Measured HBM copy bandwidth from MEASURED_PEAKS.json (driver-written);
+    fallback: the same pool's measured 6451.5 GB/s."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6451.5
+
+
+HBM_PEAK_GBPS = _hbm_peak_gbps()
+
+
 def peak_fp64_tflops(mhz=SM_MAX_MHZ):
     return N_SM * FP64_LANES * 2 * mhz * 1e6 / 1e12
 
@@ -248,6 +261,12 @@ def run_gpu(args):
         kernels["offsurface"]["fp64_pipe_frac"] = round(
             off_pairs / (off_ms / 1e3) * FP64_OPS_PER_PAIR_OFF / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)
     kernels["nbody"]["pairs_per_s"] = nb_pairs_s
+    if "self" in kernels and prof["self"][0] > 0:  # SHT stages (rows a2, a4-a6): HBM-bound by design
+        self_s = prof["self"][0] / args.steps / 1e3
+        self_bytes = 168 * N  # f, q in (48 B/node); records (96 B) + u (24 B) out
+        kernels["self"]["algorithmic_bytes"] = self_bytes
+        kernels["self"]["hbm_GBps"] = round(self_bytes / self_s / 1e9, 1)
+        kernels["self"]["hbm_frac"] = round(self_bytes / self_s / 1e9 / HBM_PEAK_GBPS, 4)
 
     # ---- e2e through the host-buffer entry points (pinned host memory)
     e2e = None
