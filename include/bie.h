@@ -226,6 +226,9 @@ int bie_reset_profile(bie_ctx* ctx);
  * surface of a sphere s (0 <= |x - c_s| - a_s < eta * 2 a_s, SPEC's
  * point-to-surface form of eq 4.5), using the exterior pressures of P:189 (S)
  * and reading R12 (D); targets inside a sphere keep the plain smooth sum.
+ * The same partition drives the traction paths (NEXT-3): bie_apply_K and
+ * bie_eval_traction use the exact traction of the source expansion (eqs
+ * 3.17-3.18) for near pairs / near exterior targets.
  * Builds the neighbour lists on the device and synchronises.  BIE_ERR_ARG for
  * eta < 0 or non-finite.
  */
