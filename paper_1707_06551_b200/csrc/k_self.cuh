@@ -5,6 +5,7 @@
 //      (x, n, w f/(8 pi mu), (3/(4 pi)) w q); rotate (a/mu) f and q to
 //      spherical components (e_r, e_theta, e_phi)
 //   B  forward real DFT over the 2p+2 azimuthal nodes of every latitude
+//      (the k <-> 2p+2-k symmetry is folded into phase A)
 //      (the FFT stage of the paper's fast transform; a dense
 //      26-point DFT at p = 12)
 //   C  Legendre projection per (density, n, m) (eq 2.3 discretised, reading
@@ -72,15 +73,20 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   const int tid = threadIdx.x, nt = blockDim.x;
 
   for (int k = tid; k < nphi; k += nt) tw[k] = make_double2(tab[L.cph + k], tab[L.sph + k]);
-  // ---------------------------------------------------------------- A
-  for (int kk = tid; kk < nsn; kk += nt) {
-    const int j = kk / nphi, k = kk - j * nphi;
+  // ---------------------------------------------------------------- A (+ B0)
+  // Node pairs (k, nphi-k) of a latitude are handled by one thread so that
+  // the real-signal symmetry used by the DFT below is applied on the fly:
+  //   C[k] = g(k) + g(nphi-k),  C[nphi-k] = g(k) - g(nphi-k)   (k = 1..p),
+  //   C[0] = g(0),  C[P1] = g(P1)  -- halving the DFT's multiply-adds.
+  const bool spec = A.self || A.alpha;
+  auto node = [&](int j, int k, double* g) {
+    const int kk = j * nphi + k;
     const int64_t i = s * nsn + kk;
     double f0 = 0, f1 = 0, f2 = 0, q0 = 0, q1 = 0, q2 = 0;
     if (A.f) { f0 = A.f[3 * i]; f1 = A.f[3 * i + 1]; f2 = A.f[3 * i + 2]; }
     if (A.q) { q0 = A.q[3 * i]; q1 = A.q[3 * i + 1]; q2 = A.q[3 * i + 2]; }
     const double ct = tab[L.t + j], st = tab[L.st + j];
-    const double cp = tab[L.cph + k], sp = tab[L.sph + k];
+    const double cp = tw[k].x, sp = tw[k].y;
     const double n0 = st * cp, n1 = st * sp, n2 = ct;
     const double w = a * a * tab[L.wu + j];
     // packed source record (row a2)
@@ -92,32 +98,38 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     r2[3] = make_double2(ws * f0, ws * f1);
     r2[4] = make_double2(ws * f2, wd * q0);
     r2[5] = make_double2(wd * q1, wd * q2);
-    if (A.self || A.alpha) {
-      // e_r = n, e_theta = (ct cp, ct sp, -st), e_phi = (-sp, cp, 0)
-      C[0 * nsn + kk] = aS * (f0 * n0 + f1 * n1 + f2 * n2);
-      C[1 * nsn + kk] = aS * (f0 * ct * cp + f1 * ct * sp - f2 * st);
-      C[2 * nsn + kk] = aS * (-f0 * sp + f1 * cp);
-      C[3 * nsn + kk] = q0 * n0 + q1 * n1 + q2 * n2;
-      C[4 * nsn + kk] = q0 * ct * cp + q1 * ct * sp - q2 * st;
-      C[5 * nsn + kk] = -q0 * sp + q1 * cp;
+    // e_r = n, e_theta = (ct cp, ct sp, -st), e_phi = (-sp, cp, 0)
+    g[0] = aS * (f0 * n0 + f1 * n1 + f2 * n2);
+    g[1] = aS * (f0 * ct * cp + f1 * ct * sp - f2 * st);
+    g[2] = aS * (-f0 * sp + f1 * cp);
+    g[3] = q0 * n0 + q1 * n1 + q2 * n2;
+    g[4] = q0 * ct * cp + q1 * ct * sp - q2 * st;
+    g[5] = -q0 * sp + q1 * cp;
+  };
+  __syncthreads();  // tw ready
+  for (int it = tid; it < P1 * (P1 + 1); it += nt) {
+    const int j = it / (P1 + 1), k = it - j * (P1 + 1);
+    const bool pair = k > 0 && k < P1;
+    double g1[6], g2[6];
+    node(j, k, g1);
+    if (pair) node(j, nphi - k, g2);
+    if (spec) {
+      double* row = C + j * nphi;
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        if (pair) {
+          row[d * nsn + k] = g1[d] + g2[d];
+          row[d * nsn + nphi - k] = g1[d] - g2[d];
+        } else {
+          row[d * nsn + k] = g1[d];
+        }
+      }
     }
   }
-  if (!A.self && !A.alpha) {
+  if (!spec) {
     if (A.u)
       for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
     return;
-  }
-  __syncthreads();
-  // ---------------------------------------------------------------- B0
-  // Real-signal symmetry of every latitude row g[k], k = 0..2p+1:
-  // in place, g[k] <- g[k] + g[nphi-k] and g[nphi-k] <- g[k] - g[nphi-k] for
-  // k = 1..p, so that the DFT below needs half the multiply-adds.
-  for (int it = tid; it < 6 * P1 * p; it += nt) {
-    const int row = it / p, k = 1 + it % p;
-    double* g = C + row * nphi;  // row = dc * P1 + j (C is [dc][j][k])
-    const double a0 = g[k], b0 = g[nphi - k];
-    g[k] = a0 + b0;
-    g[nphi - k] = a0 - b0;
   }
   __syncthreads();
   // ---------------------------------------------------------------- B
