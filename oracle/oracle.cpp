@@ -688,6 +688,20 @@ extern "C" int oracle_near(const double* centres, const double* radii, int64_t n
 // (reading R21, pinned by brute-force quadrature and the translating-sphere
 // traction in tests/test_oracle_traction.py).
 //
+// One source node k of the smooth-rule K sum at point x with normal nx
+// (eq 2.22 under the node rule of eq 4.4, reading R21):
+//   out = -(3/(4 pi)) w_k ((x-y_k).nx) ((x-y_k).sigma_k) (x-y_k) / |x-y_k|^5.
+static inline void k_pair(const double* x, const double* nx, const double* y, const double* sg,
+                          double wk, double out[3]) {
+  const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
+  const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
+  const double r5 = r2 * r2 * std::sqrt(r2);
+  const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
+  const double rs = rho[0] * sg[0] + rho[1] * sg[1] + rho[2] * sg[2];
+  const double cK = -3.0 * wk / (4.0 * PI);
+  for (int c = 0; c < 3; ++c) out[c] = cK * rn * rs * rho[c] / r5;
+}
+
 // Far field of K at the subset nodes tidx (own sphere excluded, Neumaier).
 extern "C" int oracle_far_K(const double* centres, const double* radii, int64_t ns, int p,
                             const double* sigma, const int64_t* tidx, int64_t nt, double* u) {
@@ -702,15 +716,9 @@ extern "C" int oracle_far_K(const double* centres, const double* radii, int64_t 
     Neumaier acc[3];
     for (int64_t k = 0; k < G.N; ++k) {
       if (k / G.nsn == si) continue;
-      const double* y = &G.x[3 * k];
-      const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
-      const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
-      const double r = std::sqrt(r2);
-      const double r5 = r2 * r2 * r;
-      const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
-      const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
-      const double cK = -3.0 * G.w[k] / (4.0 * PI);
-      for (int c = 0; c < 3; ++c) acc[c].add(cK * rn * rs * rho[c] / r5);
+      double v[3];
+      k_pair(x, nx, &G.x[3 * k], sigma + 3 * k, G.w[k], v);
+      for (int c = 0; c < 3; ++c) acc[c].add(v[c]);
     }
     for (int c = 0; c < 3; ++c) u[3 * t + c] = acc[c].get();
   }
@@ -729,15 +737,9 @@ extern "C" int oracle_K_at(const double* centres, const double* radii, int64_t n
     const double* nx = normals + 3 * t;
     Neumaier acc[3];
     for (int64_t k = 0; k < G.N; ++k) {
-      const double* y = &G.x[3 * k];
-      const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
-      const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
-      const double r = std::sqrt(r2);
-      const double r5 = r2 * r2 * r;
-      const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
-      const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
-      const double cK = -3.0 * G.w[k] / (4.0 * PI);
-      for (int c = 0; c < 3; ++c) acc[c].add(cK * rn * rs * rho[c] / r5);
+      double v[3];
+      k_pair(x, nx, &G.x[3 * k], sigma + 3 * k, G.w[k], v);
+      for (int c = 0; c < 3; ++c) acc[c].add(v[c]);
     }
     for (int c = 0; c < 3; ++c) u[3 * t + c] = acc[c].get();
   }
@@ -864,14 +866,9 @@ extern "C" int oracle_near_K(const double* centres, const double* radii, int64_t
       exterior_traction(p, centres + 3 * s, radii[s], AL[s], x, nx, te);
       Neumaier sm[3];
       for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
-        const double* y = &G.x[3 * k];
-        const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
-        const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
-        const double r5 = r2 * r2 * std::sqrt(r2);
-        const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
-        const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
-        const double cK = -3.0 * G.w[k] / (4.0 * PI);
-        for (int e = 0; e < 3; ++e) sm[e].add(cK * rn * rs * rho[e] / r5);
+        double v[3];
+        k_pair(x, nx, &G.x[3 * k], sigma + 3 * k, G.w[k], v);
+        for (int e = 0; e < 3; ++e) sm[e].add(v[e]);
       }
       for (int e = 0; e < 3; ++e) acc[e] += te[e] - sm[e].get();
     }
@@ -916,14 +913,9 @@ extern "C" int oracle_near_K_offsurface(const double* centres, const double* rad
       exterior_traction(p, centres + 3 * s, radii[s], AL[s], x, nx, te);
       Neumaier sm[3];
       for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
-        const double* y = &G.x[3 * k];
-        const double rho[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
-        const double r2 = rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2];
-        const double r5 = r2 * r2 * std::sqrt(r2);
-        const double rn = rho[0] * nx[0] + rho[1] * nx[1] + rho[2] * nx[2];
-        const double rs = rho[0] * sigma[3 * k] + rho[1] * sigma[3 * k + 1] + rho[2] * sigma[3 * k + 2];
-        const double cK = -3.0 * G.w[k] / (4.0 * PI);
-        for (int e = 0; e < 3; ++e) sm[e].add(cK * rn * rs * rho[e] / r5);
+        double v[3];
+        k_pair(x, nx, &G.x[3 * k], sigma + 3 * k, G.w[k], v);
+        for (int e = 0; e < 3; ++e) sm[e].add(v[e]);
       }
       for (int e = 0; e < 3; ++e) acc[e] += te[e] - sm[e].get();
     }
