@@ -48,3 +48,33 @@ def test_double_layer_of_rigid_motions_at_full_scale(bie, cfg, eta, tol):
     ctx.close()
     assert corrected <= tol, corrected
     assert plain >= 1e-6, plain                      # the correction is what makes it exact
+
+
+@pytest.mark.parametrize("gap,p,tol", [(2.0, 12, 1e-13), (1.0, 16, 1e-13), (0.5, 20, 1e-12),
+                                       (0.25, 24, 1e-12), (0.1, 30, 1e-11)])
+def test_two_sphere_drag_stimson_jeffery_gpu(bie, gap, p, tol):
+    """NEXT-1 + NEXT-2 end to end: two fixed unit spheres in a uniform flow
+    along their line of centres, BIE 5.4 solved by bie_solve_porous with the
+    near-singular correction; the drag on each sphere equals the classical
+    Stimson-Jeffery value 6 pi mu a U lambda_SJ, converging spectrally in p
+    (measured table: profiles/r01_stimson_jeffery.jsonl)."""
+    from tests.test_oracle_porous import stimson_jeffery
+    c = 1.0 + gap / 2
+    cen = np.array([[0.0, 0.0, -c], [0.0, 0.0, c]])
+    ctx = bie.bie_create(cen, np.ones(2), p, 1.0)
+    bie.bie_set_near(ctx, 10.0)
+    N = bie.bie_num_nodes(ctx)
+    uinf = torch.zeros((N, 3), dtype=torch.float64, device="cuda")
+    uinf[:, 2] = 1.0
+    mu = torch.empty_like(uinf)
+    it, res = bie.bie_solve_porous(ctx, uinf, mu, tol=1e-14, max_iter=200, restart=100)
+    w = torch.empty(N, dtype=torch.float64, device="cuda")
+    bie.bie_get_nodes(ctx, None, None, w)
+    torch.cuda.synchronize()
+    ctx.close()
+    lam = stimson_jeffery(c)
+    nsn = N // 2
+    for s in range(2):
+        F = -(w[s * nsn:(s + 1) * nsn, None] * mu[s * nsn:(s + 1) * nsn]).sum(0).cpu().numpy()
+        assert abs(F[2] / (6 * np.pi) - lam) <= tol * lam, (s, F[2] / (6 * np.pi), lam)
+        assert np.abs(F[:2]).max() <= 1e-12
