@@ -36,12 +36,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOPS_PER_PAIR = 48      # 18 DFMA (x2) + 9 DMUL + 3 DADD
-FP64_OPS_PER_PAIR = 30   # FP64-pipe instructions per pair (apply)
+# Algorithmic work per pair: 18 DFMA + 10 DMUL + 3 DADD = 31 FP64
+# operations = 49 flops (FMA = 2) for the fused SL+DL pair; the off-surface
+# pair with pressure adds 1 DADD + 1 DFMA = 33 operations = 52 flops.  (The
+# kernel itself issues 30 / 32: DESIGN.md §5.)
+FLOPS_PER_PAIR = 49
+FLOPS_PER_PAIR_OFF = 52
+FP64_OPS_PER_PAIR = 30   # FP64-pipe instructions the kernel issues per pair (apply)
 FP64_OPS_PER_PAIR_OFF = 32
 N_SM = 148
 FP64_LANES = 64          # FP64 FMA lanes per SM (B200)
 SM_MAX_MHZ = 1965.0
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
 
 
 def _hbm_peak_gbps():
@@ -58,7 +64,34 @@ HBM_PEAK_GBPS = _hbm_peak_gbps()
 
 
 def peak_fp64_tflops(mhz=SM_MAX_MHZ):
+    """Derived FP64 FMA peak (guide unit counts x clock): context only."""
     return N_SM * FP64_LANES * 2 * mhz * 1e6 / 1e12
+
+
+def measured_fp64_peak():
+    """Measured FP64 CUDA-core peak (tools/fp64_peak.cu on a B200 of this pool,
+    profiles/r02_fp64_peak.json): the best DFMA form, in TFLOP/s (FMA = 2), and
+    the FP64 operations per SM per clock it sustained at its in-kernel clock.
+    Returns (tflops, ops_per_sm_per_clk, source)."""
+    try:
+        best = None
+        with open(FP64_PEAK_FILE) as fh:
+            for line in fh:
+                line = line.strip()
+                if not line.startswith("{"):
+                    continue
+                r = json.loads(line)
+                if r.get("op", "").startswith("DFMA") and (best is None or r["tflops"] > best["tflops"]):
+                    best = r
+        if best:
+            return (float(best["tflops"]), float(best["ops_per_sm_per_clk"]),
+                    f"measured: tools/fp64_peak.cu {best['op']} "
+                    f"({os.path.relpath(FP64_PEAK_FILE, ROOT)}), {best['ops_per_s']:.4e} DFMA/s "
+                    f"at {best['sm_mhz_in_kernel']:.0f} MHz in-kernel")
+    except (OSError, KeyError, ValueError):
+        pass
+    return (peak_fp64_tflops(), float(FP64_LANES),
+            "fallback (no measured file): 148 SM x 64 FP64 lanes x 2 x 1.965 GHz")
 
 
 def max_over_ranks(value: float, world: int, device=None) -> float:
@@ -193,10 +226,16 @@ def run_gpu(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
         bie.bie_apply_SLDL(ctx, f, q, u, stream)
+        if ev:
+            ev[1].record(stream)
         if has_off:
             bie.bie_eval_offsurface(ctx, f, q, tg, uo, po, stream)
+        if ev:
+            ev[2].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -210,57 +249,74 @@ def run_gpu(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    times = []
+    times, apply_times, off_times = [], [], []
     for _ in range(args.steps):
         flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step()
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        step(ev)
+        ev[2].synchronize()
+        times.append(ev[0].elapsed_time(ev[2]))
+        apply_times.append(ev[0].elapsed_time(ev[1]))
+        off_times.append(ev[1].elapsed_time(ev[2]))
     torch.cuda.synchronize()
     clk = clocks.stop()
     prof = bie.bie_get_profile(ctx)
     bie.bie_set_profiling(ctx, False)
     total_ms = max_over_ranks(sum(times), world, dev)
+    apply_ms = max_over_ranks(sum(apply_times), world, dev)
+    off_total_ms = max_over_ranks(sum(off_times), world, dev)
     ms_per_step = total_ms / args.steps
-    value = replica_value(step_pairs, args.steps, world, total_ms)
+    # Headline: apply pairs / wall time of bie_apply_SLDL (pack +
+    # self term + far field), CUDA events on the launching stream.  The
+    # off-surface leg of the same step is reported separately ("offsurface").
+    value = replica_value(apply_pairs, args.steps, world, apply_ms)
     launches = int(sum(v[1] for k, v in prof.items() if k != "copy"))
 
-    # dominant kernel: far-field pair sum of the apply (k_nbody)
-    nb_ms = prof["nbody"][0] / args.steps
-    nb_pairs_s = apply_pairs / (nb_ms / 1e3)
-    achieved = nb_pairs_s * FLOPS_PER_PAIR / 1e12
-    peak = peak_fp64_tflops()
-    traffic = None
+    peak, peak_ops_clk, peak_src = measured_fp64_peak()
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh).get(f"cfg{args.config}")
-        if tr:
-            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            traffic_all = json.load(fh)
     except Exception:
-        pass
-    roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "traffic_note": "DRAM bytes per launch from profiles/traffic.json (ncu --set full); "
-                                "algorithmic bytes: 96 B/source record + 24 B/target = "
-                                f"{(96 + 24) * N} B",
-                "kernel": "k_nbody<8,64,64,3,false> (far-field SL+DL, row a3)",
-                "peak_source": "derived: 148 SM x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (DESIGN.md §5)",
-                "fp64_pipe_frac": round(nb_pairs_s * FP64_OPS_PER_PAIR / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)}
-    if clk.get("sm_mhz"):
-        roofline["fp64_pipe_frac_at_measured_clock"] = round(
-            nb_pairs_s * FP64_OPS_PER_PAIR / (N_SM * FP64_LANES * clk["sm_mhz"] * 1e6), 4)
+        traffic_all = {}
+
+    def kernel_roofline(kind, pairs, flops_per_pair, ops_per_pair, kname, rec_bytes, tgt_bytes,
+                        traffic_key):
+        ms = prof[kind][0] / args.steps  # ABI's CUDA events on the launching stream
+        pairs_s = pairs / (ms / 1e3)
+        achieved = pairs_s * flops_per_pair / 1e12
+        tr = traffic_all.get(traffic_key)
+        r = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+             "frac": round(achieved / peak, 4),
+             "traffic": (tr["dram_bytes_read"] + tr["dram_bytes_write"]) if tr else None,
+             "algorithmic_bytes": rec_bytes + tgt_bytes,
+             "traffic_source": (tr or {}).get("source"),
+             "kernel": kname, "ms_per_launch_avg": round(ms / max(prof[kind][1] / args.steps, 1), 4),
+             "pairs_per_s": pairs_s, "flops_per_pair": flops_per_pair,
+             "peak_source": peak_src + " (of measured)",
+             "fp64_pipe_frac_at_max_clock": round(pairs_s * ops_per_pair /
+                                                  (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)}
+        if clk.get("sm_mhz"):
+            r["fp64_pipe_frac_at_measured_clock"] = round(
+                pairs_s * ops_per_pair / (N_SM * FP64_LANES * clk["sm_mhz"] * 1e6), 4)
+        return r
+
+    # dominant kernel of the headline: the apply's far-field pair sum (k_nbody)
+    roofline = kernel_roofline("nbody", apply_pairs, FLOPS_PER_PAIR, FP64_OPS_PER_PAIR,
+                               "k_nbody<8,64,64,3,false> (far-field SL+DL, row a3)",
+                               96 * N, 24 * N, f"cfg{args.config}")
     kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
                for k, v in prof.items() if v[1]}
+    offsurface = None
     if has_off and prof["offsurface"][0] > 0:
-        off_ms = prof["offsurface"][0] / args.steps
-        kernels["offsurface"]["pairs_per_s"] = off_pairs / (off_ms / 1e3)
-        kernels["offsurface"]["fp64_pipe_frac"] = round(
-            off_pairs / (off_ms / 1e3) * FP64_OPS_PER_PAIR_OFF / (N_SM * FP64_LANES * SM_MAX_MHZ * 1e6), 4)
-    kernels["nbody"]["pairs_per_s"] = nb_pairs_s
+        roff = kernel_roofline("offsurface", off_pairs, FLOPS_PER_PAIR_OFF, FP64_OPS_PER_PAIR_OFF,
+                               "k_nbody<7,64,64,3,true> (off-surface u and p, row a7)",
+                               104 * N, 32 * M, f"cfg{args.config}_off")
+        offsurface = {"metric": "fp64 pair-interactions/sec, off-surface velocity + pressure (row a7)",
+                      "value": replica_value(off_pairs, args.steps, world, off_total_ms),
+                      "unit": "pair-interactions/s", "pairs_per_step": int(off_pairs),
+                      "n_targets": int(M), "ms_per_step": off_total_ms / args.steps,
+                      "roofline": roff}
+    kernels["nbody"]["pairs_per_s"] = roofline["pairs_per_s"]
     if "self" in kernels and prof["self"][0] > 0:  # SHT stages (rows a2, a4-a6): HBM-bound by design
         self_s = prof["self"][0] / args.steps / 1e3
         self_bytes = 168 * N  # f, q in (48 B/node); records (96 B) + u (24 B) out
@@ -274,39 +330,51 @@ def run_gpu(args):
         fh = torch.from_numpy(np.ascontiguousarray(f_np)).pin_memory()
         qh = torch.from_numpy(np.ascontiguousarray(q_np)).pin_memory()
         uh = torch.empty((N, 3), dtype=torch.float64).pin_memory()
-        h2d = 2 * N * 3 * 8
-        d2h = N * 3 * 8
+        h2d = 2 * N * 3 * 8   # f, q
+        d2h = N * 3 * 8       # u
         if has_off:
             tgh = torch.from_numpy(d["targets"]).pin_memory()
             uoh = torch.empty((M, 3), dtype=torch.float64).pin_memory()
             poh = torch.empty(M, dtype=torch.float64).pin_memory()
-            h2d += 2 * N * 3 * 8 + M * 3 * 8
-            d2h += M * 4 * 8
+            h2d_off = 2 * N * 3 * 8 + M * 3 * 8
+            d2h_off = M * 4 * 8
 
-        def step_host():
+        def step_host(ev=None):
+            if ev:
+                ev[0].record(stream)
             bie.bie_apply_SLDL_host(ctx, fh, qh, uh, stream)
+            if ev:
+                ev[1].record(stream)
             if has_off:
                 bie.bie_eval_offsurface_host(ctx, fh, qh, tgh, uoh, poh, stream)
+            if ev:
+                ev[2].record(stream)
 
         step_host()
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
-        et = []
+        ea, eo = [], []
         for _ in range(args.e2e_steps):
             flush.zero_()
             torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step_host()
-            e1.record(stream)
-            e1.synchronize()
-            et.append(e0.elapsed_time(e1))
-        tot = max_over_ranks(sum(et), world, dev)
-        e2e = {"value": replica_value(step_pairs, args.e2e_steps, world, tot), "unit": "pair-interactions/s",
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            step_host(ev)
+            ev[2].synchronize()
+            ea.append(ev[0].elapsed_time(ev[1]))
+            eo.append(ev[1].elapsed_time(ev[2]))
+        tot_a = max_over_ranks(sum(ea), world, dev)
+        e2e = {"value": replica_value(apply_pairs, args.e2e_steps, world, tot_a), "unit": "pair-interactions/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "ms_per_step": tot / args.e2e_steps}
+               "ms_per_step": tot_a / args.e2e_steps,
+               "note": "apply pairs / time of bie_apply_SLDL_host (pinned host f, q in; u out; "
+                       "H2D + D2H inside the timed region)"}
+        if has_off and offsurface is not None:
+            tot_o = max_over_ranks(sum(eo), world, dev)
+            offsurface["e2e"] = {"value": replica_value(off_pairs, args.e2e_steps, world, tot_o),
+                                 "unit": "pair-interactions/s", "h2d_bytes_per_step": h2d_off,
+                                 "d2h_bytes_per_step": d2h_off, "ms_per_step": tot_o / args.e2e_steps,
+                                 "note": "bie_eval_offsurface_host (f, q, targets in; u, p out)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -322,7 +390,8 @@ def run_gpu(args):
     out = {
         "metric": "fp64 pair-interactions/sec for SL+DL apply; % of B200 FP64 peak",
         "value": value, "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "apply_ms_per_step": apply_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json recipe, bie_inputs/)",
         "config": {"workload": f"cfg{args.config}",
@@ -330,8 +399,13 @@ def run_gpu(args):
                    "n_spheres": int(len(d["radii"])), "p": p, "n_nodes": int(N),
                    "n_offsurface_targets": int(M), "apply_pairs": int(apply_pairs),
                    "offsurface_pairs": int(off_pairs), "l2": "flushed (256 MB write) between timed steps",
+                   "value_is": "apply pairs / bie_apply_SLDL wall time (SURVEY §8(d)); "
+                               "ms_per_step is the whole step (apply + off-surface)",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": roofline,
+        "offsurface": offsurface,
+        "step_value": replica_value(step_pairs, args.steps, world, total_ms),
+        "step_value_note": "all pairs of the step (apply + off-surface) / whole-step time",
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clk,
@@ -348,17 +422,19 @@ def CONFIG_DESC(c):
 
 
 # ------------------------------------------------------------------ CPU oracle
-def cpu_baseline(d, f_np, q_np, budget_s=15.0, kind="oracle"):
+def cpu_baseline(d, f_np, q_np, budget_s=15.0, kind="oracle", legs=("apply",)):
     """Time the oracle (as it stands) on a bounded random sample of the workload:
-    batches of random target nodes (and off-surface targets) are evaluated until
-    the time budget is spent; value = pairs evaluated / wall time."""
+    batches of random target nodes of the apply (far field + self term; and,
+    with legs including "off", off-surface targets) are evaluated until the time
+    budget is spent; value = pairs evaluated / wall time (the headline metric's
+    unit: apply pairs/s)."""
     import oracle
     oracle.build_oracle()
     cores = oracle.num_threads()
     N = d["n_nodes"]
     ns = nsn_of(d["p"])
     rng = np.random.default_rng(12345)
-    has_off = d["targets"] is not None
+    has_off = d["targets"] is not None and "off" in legs
     legs = [("apply", N - ns, N)] + ([("off", N, len(d["targets"]))] if has_off else [])
     share = budget_s / len(legs)
     tot_t, tot_p, desc = 0.0, 0, []

@@ -48,7 +48,7 @@ enum bie_status {
   BIE_ERR_UNSUPPORTED = 5  /* p outside [1, BIE_P_MAX] or no sm_100a device  */
 };
 
-#define BIE_P_MAX 30 /* self-term kernel keeps one sphere's spectra in shared memory */
+#define BIE_P_MAX 32 /* 1 <= p <= 32 */
 
 /* Parts selector for bie_apply_parts (testing / measurement). */
 #define BIE_PART_FAR 1  /* smooth Nystrom sum over all other spheres (a3)  */
@@ -253,12 +253,16 @@ int64_t bie_near_pairs(const bie_ctx* ctx);
  *   Stops when the relative residual ||b - A mu|| / ||b|| <= tol or after
  *   max_iter operator applications; *iters gets the count, *rel_resid the TRUE
  *   relative residual of the returned mu (recomputed).  Not converging is
- *   not an error (check *rel_resid).  Synchronous; workspace
- *   (restart + 2) x 3N doubles is allocated per call.  1 <= restart <= 500;
+ *   not an error (check *rel_resid).  Synchronous; workspace of
+ *   (restart + 4) x 3N doubles (Krylov basis V[restart + 1], w, b, z) plus
+ *   512 x 592 + 1618 doubles of reduction partials is allocated per call and
+ *   freed before return.  Any CUDA failure inside the solve (launch, copy,
+ *   synchronisation) returns BIE_ERR_CUDA; *iters and *rel_resid are then
+ *   left untouched.  1 <= restart <= 500;
  *   restarting costs iterations (cfg 3: restart 30/50/100 -> 114/94/80
  *   iterations; cfg 5: 50 -> 200, 300 -> 138), so a restart at least as
  *   long as the expected iteration count is the better use of HBM
- *   (cfg 5: 300 vectors = 7 GB).
+ *   (cfg 5 at restart 300: 304 x 3N doubles = 7.2 GB).
  *   The force on sphere s is -sum_{k in s} w_k mu_k (Stokes drag; pinned in
  *   tests/test_oracle_porous.py).
  *   precond = 1: right preconditioning by the exact inverse of each sphere's
@@ -269,6 +273,17 @@ int64_t bie_near_pairs(const bie_ctx* ctx);
  */
 int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, int max_iter,
                      int restart, int precond, int* iters, double* rel_resid, bie_stream_t s);
+
+/*
+ * Measurement knob: which kernel computes the spectral self term (rows a2,
+ * a4-a6).  0 (default): k_sht, the batched small dense contractions on the
+ * FP64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA); 1: the same schedule
+ * with DFMA micro-kernels (compiled for p in {4, 6, 8, 12}; other orders use
+ * variant 0); 2: the round-1 one-CTA-per-sphere kernel.  All three compute the
+ * same operator (parity-tested); they differ only in schedule and speed.
+ * Returns BIE_ERR_ARG for any other value.
+ */
+int bie_set_self_kernel(bie_ctx* ctx, int variant);
 
 /*
  * Tuning knob: number of source chunks of the far-field kernel (0 = automatic;

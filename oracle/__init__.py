@@ -421,3 +421,95 @@ def offsurface_near(centres, radii, p, mu, f, q, eta, targets):
     u, pr = offsurface(centres, radii, p, mu, f, q, targets)
     du, dp = near_offsurface(centres, radii, p, mu, f, q, eta, targets)
     return u + du, pr + dp
+
+
+# ---------------------------------------------------------------- NEXT-4
+def _load_next4():
+    lib = _load()
+    if not getattr(lib, "_next4_ready", False):
+        i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        lib.oracle_next4_rotate_density.argtypes = [i32, _DP, _DP, _DP]
+        lib.oracle_vsh_project.argtypes = [i32, _DP, _DP]
+        lib.oracle_vsh_expand.argtypes = [i32, _DP, _DP, i64, _DP]
+        lib.oracle_next4_pair.argtypes = [i32, _DP, d, _DP, d, d, _DP, _DP, _DP]
+        lib.oracle_near4.argtypes = [_DP, _DP, i64, i32, d, _DP, _DP, d, _I64P, i64, _DP]
+        lib._next4_ready = True
+    return lib
+
+
+def next4_rotation(cs, ct):
+    """Q = Rz(alpha) Ry(beta) with Q e_z = (ct - cs)/|ct - cs| (reading R25);
+    the same definition as oracle.cpp's next4_rotation, for the tests."""
+    d = np.asarray(ct, dtype=np.float64) - np.asarray(cs, dtype=np.float64)
+    d = d / np.linalg.norm(d)
+    beta, alpha = np.arccos(np.clip(d[2], -1.0, 1.0)), np.arctan2(d[1], d[0])
+    ca, sa, cb, sb = np.cos(alpha), np.sin(alpha), np.cos(beta), np.sin(beta)
+    Rz = np.array([[ca, -sa, 0.0], [sa, ca, 0.0], [0.0, 0.0, 1.0]])
+    Ry = np.array([[cb, 0.0, sb], [0.0, 1.0, 0.0], [-sb, 0.0, cb]])
+    return Rz @ Ry
+
+
+def rotate_density(p, Q, g):
+    """Stage (1) of NEXT-4: gR_k = Q^T g(Q n_k) on the order-p grid, g the
+    degree-<=p expansion of the nodal density g [nsn, 3]."""
+    lib = _load_next4()
+    Q, g = _c(np.asarray(Q).reshape(9)), _c(g)
+    out = np.empty_like(g)
+    if lib.oracle_next4_rotate_density(p, _dp(Q), _dp(g), _dp(out)):
+        raise ValueError("rotate_density: bad arguments")
+    return out
+
+
+def vsh_project(p, g):
+    """Discrete VSH coefficients of a nodal density: complex [(p+1)^2, 3],
+    row n*n + n + m, columns (V, W, X)."""
+    lib = _load_next4()
+    g = _c(g)
+    out = np.empty(2 * 3 * (p + 1) ** 2)
+    if lib.oracle_vsh_project(p, _dp(g), _dp(out)):
+        raise ValueError("vsh_project: bad arguments")
+    return (out[0::2] + 1j * out[1::2]).reshape((p + 1) ** 2, 3)
+
+
+def vsh_expand(p, alpha, dirs):
+    """Re sum alpha Z(u) at unit directions dirs [M, 3] (pole-safe)."""
+    lib = _load_next4()
+    a = np.asarray(alpha, dtype=complex).reshape(-1)
+    buf = _c(np.stack([a.real, a.imag], -1).reshape(-1))
+    dirs = _c(dirs)
+    out = np.empty((len(dirs), 3))
+    if lib.oracle_vsh_expand(p, _dp(buf), _dp(dirs), len(dirs), _dp(out)):
+        raise ValueError("vsh_expand: bad arguments")
+    return out
+
+
+def next4_pair(p, cs, a_s, ct, a_t, mu, f_s, q_s):
+    """Stages (1)-(3) of PAPER §4.2 (Fig 2) for one pair: the NEXT-4 estimate
+    of S[f_s] + D[q_s] of sphere (cs, a_s) at the nodes of sphere (ct, a_t)."""
+    lib = _load_next4()
+    cs = _c(np.asarray(cs, dtype=np.float64).reshape(3))
+    ct = _c(np.asarray(ct, dtype=np.float64).reshape(3))
+    f_s, q_s = _c(f_s), _c(q_s)
+    nsn = (p + 1) * (2 * p + 2)
+    out = np.empty((nsn, 3))
+    if lib.oracle_next4_pair(p, _dp(cs), a_s, _dp(ct), a_t, mu, _dp(f_s), _dp(q_s), _dp(out)):
+        raise ValueError("next4_pair: bad arguments")
+    return out
+
+
+def near4(centres, radii, p, mu, f, q, eta, subset=None):
+    """NEXT-4 near correction du (NEXT-4 estimate minus smooth rule) at nodes `subset`."""
+    lib = _load_next4()
+    centres, radii, f, q = _c(centres), _c(radii), _c(f), _c(q)
+    N = len(radii) * (p + 1) * (2 * p + 2)
+    idx = _subset(subset, N)
+    du = np.empty((len(idx), 3))
+    if lib.oracle_near4(_dp(centres), _dp(radii), len(radii), p, mu, _dp(f), _dp(q), eta,
+                        idx.ctypes.data_as(_I64P), len(idx), _dp(du)):
+        raise ValueError("near4: bad arguments")
+    return du
+
+
+def apply_near4(centres, radii, p, mu, f, q, eta, subset=None):
+    """Composite apply with the NEXT-4 near evaluation: far + self + near4."""
+    return apply(centres, radii, p, mu, f, q, subset) + near4(centres, radii, p, mu, f, q, eta, subset)

@@ -1069,3 +1069,241 @@ extern "C" int oracle_near_offsurface(const double* centres, const double* radii
   }
   return 0;
 }
+
+// ============================================================ NEXT-4 (§4.2)
+// FFT-accelerated near evaluation with rotations (PAPER §4.2 "General case",
+// Fig 2), followed stage by stage and evaluated plainly -- no
+// Wigner matrices, no FFT: every stage is a direct evaluation of a degree-<=p
+// VSH expansion or a direct quadrature projection (eq 4.4 on the grid of eq
+// 4.2), so a reader can check each against the paper:
+//   (0) "Input: spherical harmonic coefficients of the density on the
+//       original grid": project_sphere of the source's f and q (eq 4.6).
+//   (1) "Density rotation: rotate the computational grid so that the north
+//       pole points in the direction of target center C ... equivalent
+//       coefficients for the rotated grid": Q = Rz(alpha) Ry(beta) with
+//       Q e_z = d = (c_t - c_s)/|c_t - c_s| (Euler angles (alpha, beta, 0),
+//       reading R25); the rotated-frame density sigma^R(y) = Q^T sigma(Q y) is
+//       sampled on the source grid and projected (exact: it has degree <= p).
+//   (2) "Fast evaluation at translated grid": the exterior formulas of eqs
+//       3.6-3.11 (exterior_eval) of sigma^R at the target grid of the rotated
+//       frame, x^R_jk = |c_t - c_s| e_z + a_t n_jk (discs of constant r, theta).
+//   (3) "Rotate function samples": forward transform of those samples on the
+//       target grid (project_sphere, the discrete projection of reading R9),
+//       rotated back and evaluated at the original target nodes:
+//       u(x_i) = Q u^R(Q^T n_i), with u^R the target-centred expansion.
+// The result is the degree-p re-expansion of the exact near field on the
+// target sphere (it equals the exterior field when that is band-limited and
+// converges spectrally to it as p grows); P:392's delayed evaluation (add the
+// neighbours' coefficients to the target's own, then one inverse transform)
+// changes only the rounding order, not this value.
+
+// Q = Rz(alpha) Ry(beta), Q e_z = d (row-major 3x3).
+static void next4_rotation(const double* cs, const double* ct, double Q[9]) {
+  double d[3] = {ct[0] - cs[0], ct[1] - cs[1], ct[2] - cs[2]};
+  const double L = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  for (int k = 0; k < 3; ++k) d[k] /= L;
+  const double beta = std::acos(std::max(-1.0, std::min(1.0, d[2])));
+  const double alpha = std::atan2(d[1], d[0]);
+  const double ca = std::cos(alpha), sa = std::sin(alpha), cb = std::cos(beta), sb = std::sin(beta);
+  const double Rz[9] = {ca, -sa, 0.0, sa, ca, 0.0, 0.0, 0.0, 1.0};
+  const double Ry[9] = {cb, 0.0, sb, 0.0, 1.0, 0.0, -sb, 0.0, cb};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < 3; ++k) s += Rz[3 * i + k] * Ry[3 * k + j];
+      Q[3 * i + j] = s;
+    }
+}
+
+// Cartesian V, W, X (eqs 2.4-2.6) of degree n, order m at the unit direction
+// u.  Off the poles this is vsh_cart; exactly at a pole (sin theta = 0) the
+// limits are used: Y_n^m = 0 for m != 0, and with phi = 0 there
+// d/dtheta Y_n^{+-1} = N cos(th) P_n'(cos th), (1/sin th) d/dphi Y_n^{+-1} =
+// +-i N P_n'(cos th), P_n'(+-1) = (+-1)^{n+1} n(n+1)/2; every other term 0.
+static void next4_vsh_dir(int n, int m, const double* u, cplx out[9]) {
+  const double rxy = std::sqrt(u[0] * u[0] + u[1] * u[1]);
+  if (rxy > 0.0) {
+    const double th = std::atan2(rxy, u[2]), ph = std::atan2(u[1], u[0]);
+    vsh_cart(n, m, th, ph, out);
+    return;
+  }
+  const double ct = u[2] > 0 ? 1.0 : -1.0;
+  const double er[3] = {0.0, 0.0, ct}, et[3] = {ct, 0.0, 0.0}, ep[3] = {0.0, 1.0, 0.0};
+  const double N = ynm_norm(n, m);
+  cplx Y = 0.0, dY = 0.0, dYp = 0.0;
+  if (m == 0) {
+    Y = N * ((n % 2 && ct < 0) ? -1.0 : 1.0);  // P_n(+-1) = (+-1)^n
+  } else if (std::abs(m) == 1) {
+    const double dPn = ((ct < 0 && n % 2 == 0) ? -1.0 : 1.0) * 0.5 * n * (n + 1.0);  // P_n'(+-1)
+    dY = N * ct * dPn;
+    dYp = cplx(0.0, (double)m) * N * dPn;
+  }
+  for (int c = 0; c < 3; ++c) {
+    const cplx grad = dY * et[c] + dYp * ep[c];
+    out[c] = grad - (double)(n + 1) * Y * er[c];
+    out[3 + c] = grad + (double)n * Y * er[c];
+    out[6 + c] = dY * ep[c] - dYp * et[c];
+  }
+}
+
+// Re sum_{n<=p, m, Z} alpha[(n n + n + m) 3 + ch] Z_nm(u), u a unit direction.
+static void next4_expand(int p, const std::vector<cplx>& al, const double* u, double out[3]) {
+  cplx acc[3] = {0.0, 0.0, 0.0};
+  for (int n = 0; n <= p; ++n)
+    for (int m = -n; m <= n; ++m) {
+      cplx z[9];
+      next4_vsh_dir(n, m, u, z);
+      for (int ch = 0; ch < 3; ++ch) {
+        if (n == 0 && ch > 0) continue;
+        const cplx a = al[(size_t)(n * n + n + m) * 3 + ch];
+        for (int k = 0; k < 3; ++k) acc[k] += a * z[3 * ch + k];
+      }
+    }
+  for (int k = 0; k < 3; ++k) out[k] = acc[k].real();
+}
+
+// Unit-sphere grid directions n_k of order p (node order of eq 4.2).
+static void next4_unit_grid(int p, std::vector<double>& nh) {
+  const double c0[3] = {0.0, 0.0, 0.0}, a1 = 1.0;
+  const int nsn = (p + 1) * (2 * p + 2);
+  std::vector<double> nn(3 * nsn), w(nsn);
+  nh.resize(3 * nsn);
+  oracle_nodes(c0, &a1, 1, p, nh.data(), nn.data(), w.data());
+}
+
+// Stage (1) alone: the rotated-frame density at the source grid nodes,
+// gR_k = Q^T g(Q n_k), g being the degree-<=p expansion of the nodal density g.
+extern "C" int oracle_next4_rotate_density(int p, const double* Q, const double* g, double* gR) {
+  if (p < 1 || !Q || !g || !gR) return 1;
+  std::vector<cplx> al;
+  project_sphere(p, g, al);
+  std::vector<double> nh;
+  next4_unit_grid(p, nh);
+  const int nsn = (p + 1) * (2 * p + 2);
+  for (int k = 0; k < nsn; ++k) {
+    double y[3], v[3];
+    for (int i = 0; i < 3; ++i) y[i] = Q[3 * i] * nh[3 * k] + Q[3 * i + 1] * nh[3 * k + 1] + Q[3 * i + 2] * nh[3 * k + 2];
+    next4_expand(p, al, y, v);
+    for (int i = 0; i < 3; ++i) gR[3 * k + i] = Q[i] * v[0] + Q[3 + i] * v[1] + Q[6 + i] * v[2];  // Q^T v
+  }
+  return 0;
+}
+
+// VSH coefficients of a nodal density (project_sphere), exposed for the pins:
+// alpha[(n n + n + m) 3 + ch] as (re, im) pairs, (p+1)^2 * 3 complex values.
+extern "C" int oracle_vsh_project(int p, const double* g, double* alpha_out) {
+  if (p < 1 || !g || !alpha_out) return 1;
+  std::vector<cplx> al;
+  project_sphere(p, g, al);
+  for (size_t i = 0; i < al.size(); ++i) {
+    alpha_out[2 * i] = al[i].real();
+    alpha_out[2 * i + 1] = al[i].imag();
+  }
+  return 0;
+}
+
+// Re sum alpha Z(u) at arbitrary unit directions (pole-safe), for the pins.
+extern "C" int oracle_vsh_expand(int p, const double* alpha_in, const double* dirs, int64_t m, double* out) {
+  if (p < 1 || !alpha_in || (m > 0 && (!dirs || !out))) return 1;
+  std::vector<cplx> al((size_t)(p + 1) * (p + 1) * 3);
+  for (size_t i = 0; i < al.size(); ++i) al[i] = cplx(alpha_in[2 * i], alpha_in[2 * i + 1]);
+  for (int64_t t = 0; t < m; ++t) {
+    const double* u = dirs + 3 * t;
+    const double r = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    const double uh[3] = {u[0] / r, u[1] / r, u[2] / r};
+    next4_expand(p, al, uh, out + 3 * t);
+  }
+  return 0;
+}
+
+// Stages (1)-(3) for one (source s, target t) pair: the NEXT-4 estimate of the
+// exact exterior field S[f_s] + D[q_s] of sphere s at every node of sphere t
+// (out [nsn][3]); f_s or q_s may be NULL.
+extern "C" int oracle_next4_pair(int p, const double* cs, double as, const double* ct, double at,
+                                 double mu, const double* f_s, const double* q_s, double* out) {
+  if (p < 1 || !cs || !ct || !(as > 0) || !(at > 0) || !(mu > 0) || !out) return 1;
+  const int nsn = (p + 1) * (2 * p + 2);
+  double Q[9];
+  next4_rotation(cs, ct, Q);
+  // (1) rotated-frame densities on the source grid and their coefficients
+  std::vector<double> fR, qR;
+  std::vector<cplx> afR, aqR;
+  if (f_s) {
+    fR.resize(3 * nsn);
+    oracle_next4_rotate_density(p, Q, f_s, fR.data());
+    project_sphere(p, fR.data(), afR);
+  }
+  if (q_s) {
+    qR.resize(3 * nsn);
+    oracle_next4_rotate_density(p, Q, q_s, qR.data());
+    project_sphere(p, qR.data(), aqR);
+  }
+  // (2) exterior field at the target grid of the rotated frame (source at the origin)
+  std::vector<double> nh;
+  next4_unit_grid(p, nh);
+  const double Cz = std::sqrt((ct[0] - cs[0]) * (ct[0] - cs[0]) + (ct[1] - cs[1]) * (ct[1] - cs[1]) +
+                              (ct[2] - cs[2]) * (ct[2] - cs[2]));
+  const double origin[3] = {0.0, 0.0, 0.0};
+  std::vector<double> uR(3 * nsn);
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int k = 0; k < nsn; ++k) {
+    const double x[3] = {at * nh[3 * k], at * nh[3 * k + 1], Cz + at * nh[3 * k + 2]};
+    exterior_eval(p, origin, as, mu, f_s ? &afR : nullptr, q_s ? &aqR : nullptr, x, &uR[3 * k]);
+  }
+  // (3) forward transform on the target grid, rotate back, evaluate at the nodes
+  std::vector<cplx> bR;
+  project_sphere(p, uR.data(), bR);
+  for (int k = 0; k < nsn; ++k) {
+    const double* n = &nh[3 * k];
+    double y[3], v[3];
+    for (int i = 0; i < 3; ++i) y[i] = Q[i] * n[0] + Q[3 + i] * n[1] + Q[6 + i] * n[2];  // Q^T n
+    next4_expand(p, bR, y, v);
+    for (int i = 0; i < 3; ++i) out[3 * k + i] = Q[3 * i] * v[0] + Q[3 * i + 1] * v[1] + Q[3 * i + 2] * v[2];
+  }
+  return 0;
+}
+
+// NEXT-4 near correction at the subset nodes tidx: as oracle_near, with the
+// exact exterior field of each near sphere replaced by its NEXT-4 estimate:
+// du_i = sum_{s near t} [ next4_pair(s -> t)(x_i) - smooth_s(x_i) ].
+extern "C" int oracle_near4(const double* centres, const double* radii, int64_t ns, int p, double mu,
+                            const double* f, const double* q, double eta, const int64_t* tidx,
+                            int64_t nt, double* du) {
+  if (ns < 1 || p < 1 || !(mu > 0) || !(eta >= 0) || !du || !tidx) return 1;
+  Geometry G(centres, radii, ns, p);
+  const int nsn = G.nsn;
+  // every (target sphere, near source) pair the subset touches, evaluated once
+  std::vector<int64_t> tsph;
+  for (int64_t a = 0; a < nt; ++a) tsph.push_back(tidx[a] / nsn);
+  std::sort(tsph.begin(), tsph.end());
+  tsph.erase(std::unique(tsph.begin(), tsph.end()), tsph.end());
+  std::vector<std::vector<double>> corr(tsph.size());
+  for (size_t ti = 0; ti < tsph.size(); ++ti) {
+    const int64_t t = tsph[ti];
+    corr[ti].assign(3 * nsn, 0.0);
+    for (int64_t s = 0; s < ns; ++s) {
+      if (s == t || !oracle_is_near(centres + 3 * s, radii[s], centres + 3 * t, radii[t], eta)) continue;
+      std::vector<double> ue(3 * nsn);
+      oracle_next4_pair(p, centres + 3 * s, radii[s], centres + 3 * t, radii[t], mu,
+                        f ? f + 3 * s * nsn : nullptr, q ? q + 3 * s * nsn : nullptr, ue.data());
+#pragma omp parallel for schedule(static)
+      for (int kk = 0; kk < nsn; ++kk) {
+        const int64_t i = t * nsn + kk;
+        Neumaier sm[3];
+        for (int64_t k = s * nsn; k < (s + 1) * nsn; ++k) {
+          double v[3];
+          pair_terms(&G.x[3 * i], &G.x[3 * k], &G.n[3 * k], G.w[k], f ? f + 3 * k : nullptr,
+                     q ? q + 3 * k : nullptr, mu, v, nullptr);
+          for (int c = 0; c < 3; ++c) sm[c].add(v[c]);
+        }
+        for (int c = 0; c < 3; ++c) corr[ti][3 * kk + c] += ue[3 * kk + c] - sm[c].get();
+      }
+    }
+  }
+  for (int64_t a = 0; a < nt; ++a) {
+    const int64_t t = tidx[a] / nsn;
+    const size_t ti = std::lower_bound(tsph.begin(), tsph.end(), t) - tsph.begin();
+    for (int c = 0; c < 3; ++c) du[3 * a + c] = corr[ti][3 * (tidx[a] - t * nsn) + c];
+  }
+  return 0;
+}

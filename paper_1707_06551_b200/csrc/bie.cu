@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <unordered_map>
 #include <vector>
 
@@ -17,6 +18,7 @@
 #include "k_nbody.cuh"
 #include "k_near.cuh"
 #include "k_self.cuh"
+#include "k_sht.cuh"
 #include "k_setup.cuh"
 
 using namespace bie;
@@ -61,6 +63,9 @@ struct bie_ctx {
   double* d_qn3 = nullptr;
   double* d_part = nullptr;
   size_t part_cap = 0;  // doubles
+  double* d_sht = nullptr;  // fragment-order transform tables of k_sht
+  int sht_occ = 1;          // resident k_sht CTAs per SM
+  int self_variant = 0;     // 0 k_sht DMMA, 1 k_sht DFMA, 2 round-1 k_self_t
   int chunks_override = 0;
   // near-singular correction (NEXT-1)
   double eta = 0.0;
@@ -127,13 +132,17 @@ static void prof_drain(bie_ctx* c) {
 }
 
 // ---------------------------------------------------------------- validation
-static bool is_device_ptr(const void* p) {
+// Device memory of the context's GPU (the device current at bie_create), or
+// managed memory.  Memory of another GPU is rejected here: a kernel touching it
+// would fault with a sticky error that kills the context.
+static bool is_device_ptr(const bie_ctx* c, const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  if (at.type == cudaMemoryTypeManaged) return true;
+  return at.type == cudaMemoryTypeDevice && at.device == c->dev;
 }
 
 static bool overlaps(const double* a, int64_t na, const double* b, int64_t nb) {
@@ -183,6 +192,55 @@ static bool spheres_overlap(const double* c, const double* a, int64_t n, int64_t
           }
         }
   return false;
+}
+
+// eq 4.5 for the sphere pair (s, t), evaluated in the oracle's
+// order with IEEE round-to-nearest (host x86-64 SSE2: no contraction, no
+// extended precision):  |c_s - c_t| - a_s - a_t < eta max(2 a_s, 2 a_t).
+static bool near_pair_host(const double* cs, double as, const double* ct, double at, double eta) {
+  const double dx = cs[0] - ct[0], dy = cs[1] - ct[1], dz = cs[2] - ct[2];
+  const double r2 = (dx * dx + dy * dy) + dz * dz;
+  const double d = (std::sqrt(r2) - as) - at;
+  return d < eta * std::max(2.0 * as, 2.0 * at);
+}
+
+// CSR neighbour lists of eq 4.5 (NEXT-1) with a uniform cell list, O(n):
+// a near pair has |c_s - c_t| < a_s + a_t + 2 eta a_max <= 2 a_max (1 + eta),
+// so with cells of that size (padded) every near source of t lies in the 27
+// cells around t's cell.  off is int64 (the caller bounds the total); each
+// target's sources are ascending (the order k_near accumulates in).
+static void near_lists_host(const double* c, const double* a, int64_t n, double eta,
+                            std::vector<int64_t>& off, std::vector<int>& idx) {
+  double amax = 0;
+  for (int64_t i = 0; i < n; ++i) amax = std::max(amax, a[i]);
+  const double h = 2.0 * amax * (1.0 + eta) * (1.0 + 1e-9) + 1e-300;
+  auto key = [](int64_t x, int64_t y, int64_t z) {
+    return (uint64_t)((x & 0x1FFFFF) | ((y & 0x1FFFFF) << 21) | ((z & 0x1FFFFF) << 42));
+  };
+  std::unordered_map<uint64_t, std::vector<int>> grid;
+  grid.reserve(2 * n);
+  std::vector<int64_t> cell(3 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < 3; ++d) cell[3 * i + d] = (int64_t)std::floor(c[3 * i + d] / h);
+    grid[key(cell[3 * i], cell[3 * i + 1], cell[3 * i + 2])].push_back((int)i);
+  }
+  off.assign(n + 1, 0);
+  idx.clear();
+  std::vector<int> cand;
+  for (int64_t t = 0; t < n; ++t) {
+    cand.clear();
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          auto it = grid.find(key(cell[3 * t] + dx, cell[3 * t + 1] + dy, cell[3 * t + 2] + dz));
+          if (it == grid.end()) continue;
+          for (int s : it->second)
+            if (s != t && near_pair_host(c + 3 * (int64_t)s, a[s], c + 3 * t, a[t], eta)) cand.push_back(s);
+        }
+    std::sort(cand.begin(), cand.end());
+    idx.insert(idx.end(), cand.begin(), cand.end());
+    off[t + 1] = (int64_t)idx.size();
+  }
 }
 
 // ---------------------------------------------------------------- launches
@@ -250,6 +308,18 @@ static int launch_check(bie_ctx* c, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(c, e, what);
   return BIE_OK;
+}
+
+// The self-term kernel of this context's variant: k_sht (batched DMMA or DFMA
+// contractions, default) or the round-1 per-sphere k_self_t (kept for
+// comparison; bie_set_self_kernel).
+static void self_launch(bie_ctx* c, const SelfArgs& SA, cudaStream_t s) {
+  if (c->self_variant == 2) {
+    launch_self(SA, s);
+    return;
+  }
+  const cudaError_t e = launch_sht(SA, c->d_sht, c->self_variant, c->sm_count, c->sht_occ, s);
+  (void)e;  // surfaced by the caller's launch_check (cudaGetLastError)
 }
 
 // Arguments of the per-sphere self-term kernel (k_self) for this context.
@@ -357,7 +427,7 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
       self_args(c, f, q, u, (parts & BIE_PART_SELF) ? 1 : 0, near ? c->d_alpha : nullptr, 0);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
-  launch_self(SA, s);
+  self_launch(c, SA, s);
   prof_end(c, s, &ev);
   int rc = launch_check(c, "k_self");
   if (rc) return rc;
@@ -427,7 +497,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   if (near) {  // NEXT-1 at targets: VSH projections of every sphere, then coefficients
     const SelfArgs SA = self_args(c, f, q, nullptr, 0, c->d_alpha, 0);
     prof_begin(c, BIE_KIND_SELF, s, &ev);
-    launch_self(SA, s);
+    self_launch(c, SA, s);
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_self"))) return rc;
     if ((rc = run_near_coef(c, s))) return rc;
@@ -493,7 +563,7 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
   if (near) {  // projections of sigma (q slot) -> exterior S coefficients
     const SelfArgs SA = self_args(c, nullptr, sigma, nullptr, 0, c->d_alpha, 0);
     prof_begin(c, BIE_KIND_SELF, s, &ev);
-    launch_self(SA, s);
+    self_launch(c, SA, s);
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_self"))) return rc;
     const TableLayout L(c->p);
@@ -571,7 +641,7 @@ void bie_destroy(bie_ctx* c) {
   if (!c) return;
   prof_drain(c);
   double* ptrs[] = {c->d_centres, c->d_radii, c->d_tab, c->d_x, c->d_n, c->d_w, c->d_rec,
-                    c->d_qn3, c->d_part, c->d_f, c->d_q, c->d_u, c->d_tg, c->d_uo, c->d_po};
+                    c->d_qn3, c->d_part, c->d_f, c->d_q, c->d_u, c->d_tg, c->d_uo, c->d_po, c->d_sht};
   for (double* p : ptrs)
     if (p) cudaFree(p);
   int* iptrs[] = {c->d_nb_off, c->d_nb_idx, c->d_near_tgt};
@@ -629,7 +699,7 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   bool ok = alloc(&c->d_centres, 3 * n_spheres) && alloc(&c->d_radii, n_spheres) &&
             alloc(&c->d_tab, L.total) && alloc(&c->d_x, 3 * c->N) && alloc(&c->d_n, 3 * c->N) &&
             alloc(&c->d_w, c->N) && alloc(&c->d_rec, kRec * c->N + 2 * kRec) &&
-            alloc(&c->d_qn3, c->N + 2);
+            alloc(&c->d_qn3, c->N + 2) && alloc(&c->d_sht, ShtTabLayout(p).total);
   if (!ok) {
     cudaGetLastError();
     bie_destroy(c);
@@ -646,13 +716,15 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   // row a1: GL rule -> tables -> nodes (default stream, synchronous)
   Ev ev;
   prof_begin(c, BIE_KIND_SETUP, 0, &ev);
-  k_gl_rule<<<1, 32>>>(p, c->d_tab);
+  k_gl_rule<<<1, 64>>>(p, c->d_tab);  // one thread per node, p + 1 <= 33
   k_tables<<<((p + 1) * (p + 1) + 127) / 128, 128>>>(p, c->d_tab);
   k_nodes<<<(unsigned)((c->N + 255) / 256), 256>>>(p, c->N, c->d_tab, c->d_centres, c->d_radii,
                                                   c->d_x, c->d_n, c->d_w);
-  c->launches[BIE_KIND_SETUP] += 3;
+  k_sht_tables<<<p + 5, 256>>>(p, c->d_tab, c->d_sht);
+  c->launches[BIE_KIND_SETUP] += 3;  // prof_begin counted the first of the four
   prof_end(c, 0, &ev);
   set_self_smem(p);
+  c->sht_occ = sht_prepare(p);
   // Dynamic shared memory opt-ins.  A staged near-correction variant whose
   // footprint exceeds the device limit is never launched (near_stage picks the
   // unstaged one), so it is skipped rather than requested.
@@ -711,7 +783,7 @@ int bie_get_nodes(const bie_ctx* cc, double* x, double* nrm, double* w, bie_stre
   const int64_t n[3] = {3 * c->N, 3 * c->N, c->N};
   for (int k = 0; k < 3; ++k) {
     if (!dst[k]) continue;
-    if (!is_device_ptr(dst[k])) return fail(c, BIE_ERR_ARG, "bie_get_nodes: output %s is not a device pointer", k == 0 ? "x" : (k == 1 ? "normals" : "w"));
+    if (!is_device_ptr(c, dst[k])) return fail(c, BIE_ERR_ARG, "bie_get_nodes: output %s is not a device pointer", k == 0 ? "x" : (k == 1 ? "normals" : "w"));
     cudaError_t e = cudaMemcpyAsync(dst[k], src[k], n[k] * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "bie_get_nodes");
   }
@@ -727,9 +799,9 @@ int bie_apply_parts(bie_ctx* c, const double* f, const double* q, double* u, int
     return fail(c, BIE_ERR_ARG, "parts must be a non-empty subset of FAR|SELF%s");
   if (!u) return fail(c, BIE_ERR_ARG, "u is NULL%s");
   const int64_t n3 = 3 * c->N;
-  if (!is_device_ptr(u)) return fail(c, BIE_ERR_ARG, "u is not a device pointer%s");
-  if (f && !is_device_ptr(f)) return fail(c, BIE_ERR_ARG, "f is not a device pointer%s");
-  if (q && !is_device_ptr(q)) return fail(c, BIE_ERR_ARG, "q is not a device pointer%s");
+  if (!is_device_ptr(c, u)) return fail(c, BIE_ERR_ARG, "u is not a device pointer%s");
+  if (f && !is_device_ptr(c, f)) return fail(c, BIE_ERR_ARG, "f is not a device pointer%s");
+  if (q && !is_device_ptr(c, q)) return fail(c, BIE_ERR_ARG, "q is not a device pointer%s");
   if (overlaps(u, n3, f, n3) || overlaps(u, n3, q, n3))
     return fail(c, BIE_ERR_ARG, "output u overlaps an input%s");
   return run_apply(c, f, q, u, parts, (cudaStream_t)s);
@@ -742,7 +814,7 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
   if (parts <= 0 || parts > (BIE_PART_FAR | BIE_PART_SELF | BIE_PART_COMPLETION))
     return fail(c, BIE_ERR_ARG, "parts must be a non-empty subset of FAR|SELF|COMPLETION%s");
   const int64_t n3 = 3 * c->N;
-  if (!sigma || !u || !is_device_ptr(sigma) || !is_device_ptr(u))
+  if (!sigma || !u || !is_device_ptr(c, sigma) || !is_device_ptr(c, u))
     return fail(c, BIE_ERR_ARG, "sigma and u must be device pointers%s");
   if (overlaps(u, n3, sigma, n3)) return fail(c, BIE_ERR_ARG, "output u overlaps sigma%s");
   cudaStream_t s = (cudaStream_t)st;
@@ -753,7 +825,7 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
                                 near ? c->d_alpha : nullptr, 0);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
-  launch_self(SA, s);
+  self_launch(c, SA, s);
   prof_end(c, s, &ev);
   rc = launch_check(c, "k_self");
   if (rc) return rc;
@@ -810,8 +882,8 @@ int bie_eval_offsurface(bie_ctx* c, const double* f, const double* q, const doub
   if (m < 0) return fail(c, BIE_ERR_ARG, "m < 0%s");
   if (m == 0) return BIE_OK;
   if (!tg || !u) return fail(c, BIE_ERR_ARG, "targets and u must be non-NULL%s");
-  if (!is_device_ptr(tg) || !is_device_ptr(u) || (p && !is_device_ptr(p)) ||
-      (f && !is_device_ptr(f)) || (q && !is_device_ptr(q)))
+  if (!is_device_ptr(c, tg) || !is_device_ptr(c, u) || (p && !is_device_ptr(c, p)) ||
+      (f && !is_device_ptr(c, f)) || (q && !is_device_ptr(c, q)))
     return fail(c, BIE_ERR_ARG, "a buffer is not a device pointer%s");
   const int64_t n3 = 3 * c->N;
   if (overlaps(u, 3 * m, f, n3) || overlaps(u, 3 * m, q, n3) || overlaps(u, 3 * m, tg, 3 * m) ||
@@ -830,7 +902,7 @@ int bie_eval_traction(bie_ctx* c, const double* sigma, const double* tg, const d
   if (m == 0) return BIE_OK;
   if (!sigma || !tg || !tn || !t)
     return fail(c, BIE_ERR_ARG, "sigma, targets, normals and t must be non-NULL%s");
-  if (!is_device_ptr(sigma) || !is_device_ptr(tg) || !is_device_ptr(tn) || !is_device_ptr(t))
+  if (!is_device_ptr(c, sigma) || !is_device_ptr(c, tg) || !is_device_ptr(c, tn) || !is_device_ptr(c, t))
     return fail(c, BIE_ERR_ARG, "a buffer is not a device pointer%s");
   if (overlaps(t, 3 * m, sigma, 3 * c->N) || overlaps(t, 3 * m, tg, 3 * m) ||
       overlaps(t, 3 * m, tn, 3 * m))
@@ -969,30 +1041,24 @@ int bie_set_near(bie_ctx* c, double eta) {
   c->eta = eta;
   if (eta == 0.0) return BIE_OK;
   const int64_t ns = c->ns;
-  int* d_cnt = nullptr;
-  if (cudaMalloc(&d_cnt, ns * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&c->d_nb_off, (ns + 1) * sizeof(int)) != cudaSuccess) {
-    cudaGetLastError();
-    cudaFree(d_cnt);
-    near_free(c);
-    return fail(c, BIE_ERR_ALLOC, "near lists%s");
-  }
-  const unsigned g = (unsigned)((ns + 127) / 128);
-  k_near_lists<<<g, 128>>>(ns, c->d_centres, c->d_radii, eta, d_cnt, nullptr, nullptr);
-  std::vector<int> cnt(ns), off(ns + 1, 0), tgt;
-  if (cudaMemcpy(cnt.data(), d_cnt, ns * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {
+  // Host-side copies of the geometry (bie_create keeps only device copies).
+  std::vector<double> hc(3 * ns), ha(ns);
+  if (cudaMemcpy(hc.data(), c->d_centres, 3 * ns * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(ha.data(), c->d_radii, ns * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
     cudaError_t e = cudaGetLastError();
-    cudaFree(d_cnt);
-    near_free(c);
-    return cuda_fail(c, e, "bie_set_near: neighbour counts");
+    return cuda_fail(c, e, "bie_set_near: geometry");
   }
-  for (int64_t t = 0; t < ns; ++t) {
-    off[t + 1] = off[t] + cnt[t];
-    if (cnt[t]) tgt.push_back((int)t);
-  }
+  std::vector<int64_t> off;
+  std::vector<int> idx, tgt;
+  near_lists_host(hc.data(), ha.data(), ns, eta, off, idx);
+  if (off[ns] > (int64_t)INT32_MAX)
+    return fail(c, BIE_ERR_UNSUPPORTED, "bie_set_near: more than 2^31-1 near pairs%s");
+  std::vector<int> off32(ns + 1);
+  for (int64_t t = 0; t <= ns; ++t) off32[t] = (int)off[t];
+  for (int64_t t = 0; t < ns; ++t)
+    if (off[t + 1] > off[t]) tgt.push_back((int)t);
   c->n_near_pairs = off[ns];
   c->n_near_tgt = (int)tgt.size();
-  cudaFree(d_cnt);
   const TableLayout L(c->p);
   if (cudaMalloc(&c->d_alpha, (size_t)ns * 12 * L.nlm * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->d_ncoef, (size_t)ns * 10 * L.nlm * sizeof(double)) != cudaSuccess) {
@@ -1000,25 +1066,21 @@ int bie_set_near(bie_ctx* c, double eta) {
     near_free(c);
     return fail(c, BIE_ERR_ALLOC, "near coefficients%s");
   }
-  if (c->n_near_pairs == 0) return launch_check(c, "k_near_lists");
-  if (cudaMalloc(&c->d_nb_idx, off[ns] * sizeof(int)) != cudaSuccess ||
+  if (c->n_near_pairs == 0) return BIE_OK;
+  if (cudaMalloc(&c->d_nb_off, (ns + 1) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->d_nb_idx, idx.size() * sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->d_near_tgt, tgt.size() * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     near_free(c);
     return fail(c, BIE_ERR_ALLOC, "near lists%s");
   }
-  if (cudaMemcpy(c->d_nb_off, off.data(), (ns + 1) * sizeof(int), cudaMemcpyHostToDevice) !=
-          cudaSuccess ||
-      cudaMemcpy(c->d_near_tgt, tgt.data(), tgt.size() * sizeof(int), cudaMemcpyHostToDevice) !=
-          cudaSuccess) {
+  if (cudaMemcpy(c->d_nb_off, off32.data(), (ns + 1) * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c->d_nb_idx, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c->d_near_tgt, tgt.data(), tgt.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
     cudaError_t e = cudaGetLastError();
     near_free(c);
     return cuda_fail(c, e, "bie_set_near: lists");
   }
-  k_near_lists<<<g, 128>>>(ns, c->d_centres, c->d_radii, eta, nullptr, c->d_nb_off, c->d_nb_idx);
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(c, e, "bie_set_near");
   return BIE_OK;
 }
 
@@ -1031,16 +1093,26 @@ struct Krylov {
   cudaStream_t s;
   int64_t n;
   double* part = nullptr;  // [kDotBlocks + 1]
+  // First CUDA error seen by any Krylov step (launch, copy or synchronisation).
+  // A failed step leaves its host-side result undefined, so every caller checks
+  // `ok()` before using one (no false "converged" after a fault).
+  cudaError_t err = cudaSuccess;
+  void note(cudaError_t e) {
+    if (e != cudaSuccess && err == cudaSuccess) err = e;
+  }
+  void note_launch() { note(cudaGetLastError()); }
+  bool ok() const { return err == cudaSuccess; }
   double dot(const double* x, const double* y) {
     Ev ev;
     prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
     k_dot_partial<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, y, part);
     k_dot_final<<<1, kDotThreads, 0, s>>>(part, part + kDotBlocks);
     prof_end(c, s, &ev);
+    note_launch();
     double h = 0.0;
-    cudaMemcpyAsync(&h, part + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    return h;
+    note(cudaMemcpyAsync(&h, part + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
+    note(cudaStreamSynchronize(s));
+    return ok() ? h : std::nan("");
   }
   // classical Gram-Schmidt twice against V[0..nv): on return hv[0..nv) holds
   // the projections (device), w is orthogonalised, and wnorm2 = w.w; one sync.
@@ -1055,9 +1127,10 @@ struct Krylov {
     k_dot_partial<<<kDotBlocks, kDotThreads, 0, s>>>(n, w, w, part);
     k_dot_final<<<1, kDotThreads, 0, s>>>(part, dh + 1024);
     prof_end(c, s, &ev);
-    std::vector<double> hh(1025);
-    cudaMemcpyAsync(hh.data(), dh, 1025 * sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    note_launch();
+    std::vector<double> hh(1025, std::nan(""));
+    note(cudaMemcpyAsync(hh.data(), dh, 1025 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    note(cudaStreamSynchronize(s));
     for (int i = 0; i < nv; ++i) hv[i] = hh[i] + hh[512 + i];
     *wnorm2 = hh[1024];
   }
@@ -1067,13 +1140,18 @@ struct Krylov {
     prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
     k_axpby<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, x, b, y);
     prof_end(c, s, &ev);
+    note_launch();
   }
+  void copy(double* dst, const double* src) {
+    note(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  void zero(double* dst) { note(cudaMemsetAsync(dst, 0, n * sizeof(double), s)); }
   // y = P^{-1} x, P = 1/2 I + S_self + D_self (block diagonal, exact via the spectra)
   int prec(const double* x, double* y) {
     const SelfArgs SA = self_args(c, nullptr, x, y, 1, nullptr, 1);
     Ev ev;
     prof_begin(c, BIE_KIND_KRYLOV, s, &ev);
-    launch_self(SA, s);
+    self_launch(c, SA, s);
     prof_end(c, s, &ev);
     return launch_check(c, "k_self(precond)");
   }
@@ -1082,7 +1160,7 @@ struct Krylov {
     int rc = run_apply(c, x, x, y, BIE_PART_FAR | BIE_PART_SELF, s);
     if (rc) return rc;
     axpby(0.5, x, 1.0, y);
-    return launch_check(c, "k_axpby");
+    return ok() ? BIE_OK : cuda_fail(c, err, "bie_solve_porous: k_axpby");
   }
 };
 }  // namespace
@@ -1093,7 +1171,7 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
   if (!c) return BIE_ERR_ARG;
   int rc = check_device(c);
   if (rc) return rc;
-  if (!uinf || !mu_out || !is_device_ptr(uinf) || !is_device_ptr(mu_out))
+  if (!uinf || !mu_out || !is_device_ptr(c, uinf) || !is_device_ptr(c, mu_out))
     return fail(c, BIE_ERR_ARG, "uinf and mu must be device pointers%s");
   const int64_t n = 3 * c->N;
   if (overlaps(uinf, n, mu_out, n)) return fail(c, BIE_ERR_ARG, "mu overlaps uinf%s");
@@ -1120,12 +1198,16 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
     cudaFree(K.part);
   };
   // b = -u_inf, x0 = 0
-  cudaMemsetAsync(mu_out, 0, n * sizeof(double), K.s);
-  cudaMemsetAsync(b, 0, n * sizeof(double), K.s);
+  K.zero(mu_out);
+  K.zero(b);
   K.axpby(-1.0, uinf, 0.0, b);
   const double bnorm = std::sqrt(K.dot(b, b));
   int it = 0;
   double rel = 0.0;
+  if (!K.ok()) {
+    cleanup();
+    return cuda_fail(c, K.err, "bie_solve_porous: setup");
+  }
   if (bnorm == 0.0) {
     cleanup();
     if (iters_out) *iters_out = 0;
@@ -1138,9 +1220,10 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
     // r = b - A x  -> V[0]
     double* v0 = V;
     if ((rc = K.op(mu_out, w))) { cleanup(); return rc; }
-    cudaMemcpyAsync(v0, b, n * sizeof(double), cudaMemcpyDeviceToDevice, K.s);
+    K.copy(v0, b);
     K.axpby(-1.0, w, 1.0, v0);
     const double beta = std::sqrt(K.dot(v0, v0));
+    if (!K.ok()) { cleanup(); return cuda_fail(c, K.err, "bie_solve_porous: residual"); }
     rel = beta / bnorm;
     if (rel <= tol || it >= max_iter) break;
     K.axpby(0.0, v0, 1.0 / beta, v0);
@@ -1160,6 +1243,7 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
       std::vector<double> hcol(j + 1);
       double wn2 = 0.0;
       K.cgs2(V, j + 1, vn, dh, hcol.data(), &wn2);
+      if (!K.ok()) { cleanup(); return cuda_fail(c, K.err, "bie_solve_porous: Arnoldi"); }
       for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i];
       const double hn = std::sqrt(wn2);
       H[(size_t)(j + 1) * m + j] = hn;
@@ -1192,7 +1276,7 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
       y[i] = sacc / H[(size_t)i * m + i];
     }
     if (precond) {  // mu += P^{-1} (V y)
-      cudaMemsetAsync(w, 0, n * sizeof(double), K.s);
+      K.zero(w);
       for (int i = 0; i < j; ++i) K.axpby(y[i], V + (size_t)i * n, 1.0, w);
       if ((rc = K.prec(w, z))) { cleanup(); return rc; }
       K.axpby(1.0, z, 1.0, mu_out);
@@ -1206,10 +1290,18 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
   K.axpby(1.0, b, -1.0, w);
   rel = std::sqrt(K.dot(w, w)) / bnorm;
   cleanup();
-  if (iters_out) *iters_out = it;
-  if (resid_out) *resid_out = rel;
+  if (!K.ok()) return cuda_fail(c, K.err, "bie_solve_porous");
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(c, e, "bie_solve_porous");
+  if (iters_out) *iters_out = it;
+  if (resid_out) *resid_out = rel;
+  return BIE_OK;
+}
+
+int bie_set_self_kernel(bie_ctx* c, int variant) {
+  if (!c) return BIE_ERR_ARG;
+  if (variant < 0 || variant > 2) return fail(c, BIE_ERR_ARG, "self kernel variant must be 0, 1 or 2%s");
+  c->self_variant = variant;
   return BIE_OK;
 }
 

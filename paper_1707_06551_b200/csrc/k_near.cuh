@@ -19,34 +19,6 @@
 
 namespace bie {
 
-// eq 4.5 with IEEE round-to-nearest in the oracle's evaluation order.
-__device__ __forceinline__ bool near_pair(const double* cs, double as, const double* ct, double at,
-                                          double eta) {
-  const double dx = __dsub_rn(cs[0], ct[0]), dy = __dsub_rn(cs[1], ct[1]),
-               dz = __dsub_rn(cs[2], ct[2]);
-  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  const double d = __dsub_rn(__dsub_rn(__dsqrt_rn(r2), as), at);
-  return d < __dmul_rn(eta, fmax(__dmul_rn(2.0, as), __dmul_rn(2.0, at)));
-}
-
-// CSR neighbour lists: pass 0 counts, pass 1 fills (ascending source index).
-__global__ void k_near_lists(int64_t ns, const double* __restrict__ centres,
-                             const double* __restrict__ radii, double eta, int* __restrict__ cnt,
-                             const int* __restrict__ off, int* __restrict__ idx) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= ns) return;
-  int c = 0;
-  int o = off ? off[t] : 0;
-  for (int64_t s = 0; s < ns; ++s) {
-    if (s == t) continue;
-    if (near_pair(centres + 3 * s, radii[s], centres + 3 * t, radii[t], eta)) {
-      if (idx) idx[o + c] = (int)s;
-      ++c;
-    }
-  }
-  if (cnt) cnt[t] = c;
-}
-
 struct NearArgs {
   int p, nsn;
   const double* tab;

@@ -45,10 +45,11 @@ struct SelfArgs {
 
 __host__ __device__ inline int64_t self_smem_doubles(int p) {
   const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
-  const int64_t C = 6LL * nsn;                    // spherical components; reused as U
-  const int64_t F = 12LL * P1 * P1;               // [2 dens][3 comp][j][m][re,im]
-  const int64_t PSI = 6LL * (P1 * (P1 + 1) / 2);  // [(n,m)][Y,G,X][re,im]
-  return C + F + PSI + 2LL * nphi;
+  const int64_t C = 6LL * nsn;       // spherical components; reused as ALPHA, then U
+  const int64_t F = 12LL * P1 * P1;  // [2 dens][3 comp][j][m][re,im]; reused as PSI
+  // PSI ([(n,m)][Y,G,X][re,im], 3 P1 (P1+1) <= F doubles) aliases F, dead after
+  // phase C: 24 P1^2 + 4 P1 doubles = 210 KB at p = 32 (<= 227 KB opt-in).
+  return C + F + 2LL * nphi;
 }
 
 // PT > 0: the order p is the compile-time constant PT (loop bounds, index
@@ -61,8 +62,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   const int nlm = L.nlm;
   double* C = sm;                          // [2][3][nsn]
   double* F = C + 6 * nsn;                 // [2][3][P1][P1][2]
-  double* PSI = F + 12 * P1 * P1;          // [nlm][3][2]
-  double2* tw = reinterpret_cast<double2*>(PSI + 6 * nlm);  // (cos, sin)(2 pi q/nphi)
+  double* PSI = F;                         // [nlm][3][2]; aliases F (dead after phase C)
+  double2* tw = reinterpret_cast<double2*>(F + 12 * P1 * P1);  // (cos, sin)(2 pi q/nphi)
   double* U = C;                           // [3][P1][P1][2] (C is dead after B)
   const double* __restrict__ tab = A.tab;
   const int64_t s = blockIdx.x;

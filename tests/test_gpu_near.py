@@ -170,7 +170,7 @@ def test_offsurface_near_config5_subset(bie, oracle_mod):
     _assert_parity(pr.cpu().numpy()[tsub], pref, "cfg5 near p")
 
 
-@pytest.mark.parametrize("p", [24, 30])
+@pytest.mark.parametrize("p", [24, 30, 32])
 def test_near_high_order_unstaged(bie, oracle_mod, p):
     """p >= 24: a neighbour's records + coefficients no longer fit the 160 KB
     staging budget, so k_near reads them from global memory (the STAGE = false

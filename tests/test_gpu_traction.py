@@ -56,7 +56,7 @@ def test_K_config3_subset(bie, oracle_mod):
     _assert_parity(got, oracle_mod.apply_K(d["centres"], d["radii"], d["p"], f, sub), "cfg3 K")
 
 
-@pytest.mark.parametrize("p,ns", [(3, 2), (6, 9), (12, 4), (30, 2)])
+@pytest.mark.parametrize("p,ns", [(3, 2), (6, 9), (12, 4), (30, 2), (32, 2)])
 def test_completion_matches_oracle(bie, oracle_mod, p, ns):
     """Completion L of eq 5.8 (reading R22), alone and with K_pv; p = 30
     exercises nsn = 1,922 > the CTA width (strided per-thread sums)."""
