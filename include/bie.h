@@ -67,7 +67,8 @@ enum bie_status {
 #define BIE_KIND_KRYLOV 8   /* GMRES vector kernels (NEXT-2)                  */
 #define BIE_KIND_KFAR 9     /* far-field traction operator K pair sum (NEXT-3) */
 #define BIE_KIND_COMPLETE 10 /* completion operator L of eq 5.8 (NEXT-3)          */
-#define BIE_NUM_KINDS 11
+#define BIE_KIND_NEAR4 11   /* rotated near evaluation of PAPER §4.2 (NEXT-4)    */
+#define BIE_NUM_KINDS 12
 
 /*
  * bie_create -- build nodes, weights, normals and spectral tables (row a1).
@@ -275,6 +276,30 @@ int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, i
                      int restart, int precond, int* iters, double* rel_resid, bie_stream_t s);
 
 /*
+ * bie_set_near_mode -- how the near-singular correction of bie_set_near
+ * evaluates the exact exterior field of a near source sphere s at the nodes of
+ * a target sphere t (velocity applies: bie_apply_SL/DL/SLDL/parts):
+ *   0 (default) direct (NEXT-1): the exterior expansion of eqs 3.6-3.11
+ *     evaluated at every node of t, O(p^4) per pair.
+ *   1 rotated (NEXT-4, PAPER §4.2 "General case", Fig 2): s's
+ *     coefficients are rotated into the frame whose pole points at c_t
+ *     (Wigner-type rotation through a fixed per-degree matrix, reading R25),
+ *     evaluated on t's pole-aligned discs (eq 4.8; eq 4.9's geometry),
+ *     re-expanded in t's vector spherical harmonics, rotated back and
+ *     accumulated with t's own coefficients before the self term's single
+ *     inverse transform, O(p^3) per pair.  The result is the degree-p
+ *     re-expansion of the exact near field on t (it differs from mode 0 by
+ *     the degree > p tail of that field, which decays spectrally with p).
+ *   2, 3: measurement only -- the exterior part alone (mode 0's and mode 1's
+ *     respectively), without the smooth-rule subtraction; not an operator.
+ * Modes 1 and 3 build a (p+1)(2p+1)(2p+3)/3-entry complex table and an
+ * [n_spheres][nlm][6] coefficient buffer on the first call (synchronous).
+ * The traction operator and the off-surface evaluators always use mode 0.
+ * Returns BIE_ERR_ARG for other modes.
+ */
+int bie_set_near_mode(bie_ctx* ctx, int mode);
+
+/*
  * Measurement knob: which kernel computes the spectral self term (rows a2,
  * a4-a6).  0 (default): k_sht, the batched small dense contractions on the
  * FP64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA); 1: the same schedule
@@ -284,6 +309,19 @@ int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, i
  * Returns BIE_ERR_ARG for any other value.
  */
 int bie_set_self_kernel(bie_ctx* ctx, int variant);
+
+/*
+ * Measurement knob: how the far-field kernels combine their source chunks.
+ * 0 (default): chunk partials in HBM, summed by a fixed-order reduction
+ * kernel.  1 / 2 / 3: when the launch is large enough (>= 16 units per
+ * resident CTA slot), the source chunks of a target tile run as ONE
+ * thread-block cluster of 8 / 4 / 16 CTAs (16: apply only, non-portable size)
+ * and are summed on chip through distributed shared memory in fixed rank
+ * order -- no partials in HBM, no reduction launch; smaller launches keep the
+ * HBM path.  All are deterministic; they differ only in fp64 summation
+ * grouping.  BIE_ERR_ARG outside 0..3.
+ */
+int bie_set_far_reduction(bie_ctx* ctx, int mode);
 
 /*
  * Tuning knob: number of source chunks of the far-field kernel (0 = automatic;

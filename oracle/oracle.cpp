@@ -1116,28 +1116,40 @@ static void next4_rotation(const double* cs, const double* ct, double Q[9]) {
 }
 
 // Cartesian V, W, X (eqs 2.4-2.6) of degree n, order m at the unit direction
-// u.  Off the poles this is vsh_cart; exactly at a pole (sin theta = 0) the
-// limits are used: Y_n^m = 0 for m != 0, and with phi = 0 there
-// d/dtheta Y_n^{+-1} = N cos(th) P_n'(cos th), (1/sin th) d/dphi Y_n^{+-1} =
-// +-i N P_n'(cos th), P_n'(+-1) = (+-1)^{n+1} n(n+1)/2; every other term 0.
+// u, pole-safe: with x = cos th = u_z, s = sin th = |(u_x, u_y)| (never from
+// sqrt(1 - x^2)) and Pb = P_n^|m| / s^|m| (a polynomial in x; no
+// Condon-Shortley phase, eq 2.1):
+//   Pb_m^m = (2m-1)!!, Pb_{m+1}^m = (2m+1) x Pb_m^m,
+//   (n-m) Pb_n^m = (2n-1) x Pb_{n-1}^m - (n+m-1) Pb_{n-2}^m   (and d/dx of it),
+//   Y = N Pb s^m e^{i m ph},  (1/s) dY/dph = i m N Pb s^{m-1} e^{i m ph},
+//   dY/dth = N s^{m-1} (m x Pb - s^2 dPb/dx) e^{i m ph};
+// no division by s, so a direction on (or rounding onto) the polar axis is exact.
 static void next4_vsh_dir(int n, int m, const double* u, cplx out[9]) {
-  const double rxy = std::sqrt(u[0] * u[0] + u[1] * u[1]);
-  if (rxy > 0.0) {
-    const double th = std::atan2(rxy, u[2]), ph = std::atan2(u[1], u[0]);
-    vsh_cart(n, m, th, ph, out);
-    return;
+  const int am = std::abs(m);
+  const double x = u[2], s = std::sqrt(u[0] * u[0] + u[1] * u[1]);
+  const double ph = std::atan2(u[1], u[0]);
+  double pb = 1.0;
+  for (int k = 1; k <= am; ++k) pb *= (2.0 * k - 1.0);  // (2m-1)!!
+  double p0 = 0.0, p1 = pb, d0 = 0.0, d1 = 0.0;         // Pb_{m-1} = 0
+  for (int l = am + 1; l <= n; ++l) {
+    const double p2 = ((2.0 * l - 1.0) * x * p1 - (l + am - 1.0) * p0) / (l - am);
+    const double d2 = ((2.0 * l - 1.0) * (p1 + x * d1) - (l + am - 1.0) * d0) / (l - am);
+    p0 = p1; p1 = p2; d0 = d1; d1 = d2;
   }
-  const double ct = u[2] > 0 ? 1.0 : -1.0;
-  const double er[3] = {0.0, 0.0, ct}, et[3] = {ct, 0.0, 0.0}, ep[3] = {0.0, 1.0, 0.0};
+  const double sm1 = am >= 1 ? std::pow(s, am - 1) : 0.0;  // s^{m-1} (unused for m = 0)
   const double N = ynm_norm(n, m);
-  cplx Y = 0.0, dY = 0.0, dYp = 0.0;
-  if (m == 0) {
-    Y = N * ((n % 2 && ct < 0) ? -1.0 : 1.0);  // P_n(+-1) = (+-1)^n
-  } else if (std::abs(m) == 1) {
-    const double dPn = ((ct < 0 && n % 2 == 0) ? -1.0 : 1.0) * 0.5 * n * (n + 1.0);  // P_n'(+-1)
-    dY = N * ct * dPn;
-    dYp = cplx(0.0, (double)m) * N * dPn;
+  const cplx e = std::polar(1.0, m * ph);
+  const cplx Y = N * p1 * std::pow(s, am) * e;
+  cplx dY, dYp;
+  if (am == 0) {
+    dY = N * (-s * d1) * e;  // d/dth P_n(cos th) = -s P_n'(x)
+    dYp = 0.0;
+  } else {
+    dY = N * sm1 * (am * x * p1 - s * s * d1) * e;
+    dYp = cplx(0.0, (double)m) * N * p1 * sm1 * e;
   }
+  const double cp = std::cos(ph), sp = std::sin(ph);
+  const double er[3] = {s * cp, s * sp, x}, et[3] = {x * cp, x * sp, -s}, ep[3] = {-sp, cp, 0.0};
   for (int c = 0; c < 3; ++c) {
     const cplx grad = dY * et[c] + dYp * ep[c];
     out[c] = grad - (double)(n + 1) * Y * er[c];

@@ -13,7 +13,8 @@ LIB_PATH = os.path.join(_HERE, "libbie.so")
 BIE_OK, BIE_ERR_ARG, BIE_ERR_GEOMETRY, BIE_ERR_ALLOC, BIE_ERR_CUDA, BIE_ERR_UNSUPPORTED = range(6)
 BIE_P_MAX = 32
 BIE_PART_FAR, BIE_PART_SELF, BIE_PART_COMPLETION = 1, 2, 4
-KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov", "kfar", "complete")
+KINDS = ("setup", "self", "pack", "nbody", "reduce", "offsurface", "copy", "near", "krylov", "kfar", "complete",
+         "near4")
 BIE_NUM_KINDS = len(KINDS)
 
 #: every symbol include/bie.h declares (checked by tests/test_abi_cpu.py)
@@ -22,7 +23,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
-    "bie_set_self_kernel",
+    "bie_set_self_kernel", "bie_set_near_mode", "bie_set_far_reduction",
     "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K", "bie_eval_traction",
     "bie_status_string", "bie_last_error",
 )
@@ -55,6 +56,8 @@ _lib.bie_get_profile.argtypes = [_vp, _DP, ctypes.POINTER(_i64)]
 _lib.bie_reset_profile.argtypes = [_vp]
 _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
 _lib.bie_set_self_kernel.argtypes = [_vp, _i32]
+_lib.bie_set_near_mode.argtypes = [_vp, _i32]
+_lib.bie_set_far_reduction.argtypes = [_vp, _i32]
 _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
 _lib.bie_near_pairs.restype = _i64
@@ -277,6 +280,17 @@ def bie_set_self_kernel(ctx, variant: int):
     """Self-term kernel: 0 batched DMMA contractions (default), 1 batched DFMA,
     2 the round-1 one-CTA-per-sphere kernel (include/bie.h)."""
     _check(ctx, _lib.bie_set_self_kernel(ctx.handle, int(variant)))
+
+
+def bie_set_far_reduction(ctx, mode: int):
+    """0: cluster (DSMEM) reduction of source chunks when large enough; 1: HBM partials + k_reduce."""
+    _check(ctx, _lib.bie_set_far_reduction(ctx.handle, int(mode)))
+
+
+def bie_set_near_mode(ctx, mode: int):
+    """Near evaluation: 0 direct (NEXT-1), 1 rotated (NEXT-4, PAPER §4.2);
+    2 / 3 measurement only (exterior part alone), include/bie.h."""
+    _check(ctx, _lib.bie_set_near_mode(ctx.handle, int(mode)))
 
 
 def bie_set_near(ctx, eta: float):

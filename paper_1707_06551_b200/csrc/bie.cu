@@ -16,6 +16,7 @@
 #include "k_complete.cuh"
 #include "k_krylov.cuh"
 #include "k_nbody.cuh"
+#include "k_n4.cuh"
 #include "k_near.cuh"
 #include "k_self.cuh"
 #include "k_sht.cuh"
@@ -40,6 +41,14 @@ constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 #define NBODY_OFF k_nbody<kR_OFF, kTPB, kTS, kNST, true, 1, 2>
 #define NBODY_K k_nbody<kR_K, kTPB, kTS, kNST, false, 1, 2, 1>
 #define NBODY_OFFK k_nbody<kR_OFFK, kTPB, kTS, kNST, true, 1, 2, 1>
+// cluster-reduced variants (source chunks of a target tile = one cluster)
+constexpr int kCL = 8;
+#define NBODY_APPLY_CL k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, kCL>
+#define NBODY_APPLY_CL4 k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, 4>
+#define NBODY_APPLY_CL16 k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, 16>
+#define NBODY_OFF_CL k_nbody<kR_OFF, kTPB, kTS, kNST, true, 1, 2, 0, kCL>
+#define NBODY_K_CL k_nbody<kR_K, kTPB, kTS, kNST, false, 1, 2, 1, kCL>
+#define NBODY_OFFK_CL k_nbody<kR_OFFK, kTPB, kTS, kNST, true, 1, 2, 1, kCL>
 
 struct Ev {
   int kind;
@@ -67,6 +76,7 @@ struct bie_ctx {
   int sht_occ = 1;          // resident k_sht CTAs per SM
   int self_variant = 0;     // 0 k_sht DMMA, 1 k_sht DFMA, 2 round-1 k_self_t
   int chunks_override = 0;
+  int far_red = 0;  // bie_set_far_reduction: 0 HBM partials + k_reduce; 1/2/3 clusters of 8/4/16
   // near-singular correction (NEXT-1)
   double eta = 0.0;
   int n_near_tgt = 0;
@@ -76,6 +86,10 @@ struct bie_ctx {
   int* d_near_tgt = nullptr;
   double* d_alpha = nullptr;
   double* d_ncoef = nullptr;
+  // NEXT-4 (bie_set_near_mode): 0 direct, 1 rotated (PAPER §4.2), 2/3 measurement
+  int near_mode = 0;
+  double* d_delta = nullptr;    // packed Delta_n (rotation operator of T = Rx(-pi/2))
+  double* d_psinear = nullptr;  // [ns][nlm][6] accumulated neighbour coefficients
   // staging for the _host entry points
   double *d_f = nullptr, *d_q = nullptr, *d_u = nullptr;
   double *d_tg = nullptr, *d_uo = nullptr, *d_po = nullptr;
@@ -314,11 +328,13 @@ static int launch_check(bie_ctx* c, const char* what) {
 // contractions, default) or the round-1 per-sphere k_self_t (kept for
 // comparison; bie_set_self_kernel).
 static void self_launch(bie_ctx* c, const SelfArgs& SA, cudaStream_t s) {
-  if (c->self_variant == 2) {
+  if (c->self_variant == 2 && !SA.psinear) {
     launch_self(SA, s);
     return;
   }
-  const cudaError_t e = launch_sht(SA, c->d_sht, c->self_variant, c->sm_count, c->sht_occ, s);
+  // (NEXT-4's coefficient accumulation exists only in k_sht)
+  const cudaError_t e = launch_sht(SA, c->d_sht, c->self_variant == 2 ? 0 : c->self_variant, c->sm_count,
+                                   c->sht_occ, s);
   (void)e;  // surfaced by the caller's launch_check (cudaGetLastError)
 }
 
@@ -358,7 +374,7 @@ static int run_near_coef(bie_ctx* c, cudaStream_t s) {
 
 // Near correction at the nodes (NEXT-1 velocity, K = false; NEXT-3 traction,
 // K = true), after the far field: one CTA per target sphere with neighbours.
-static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K) {
+static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K, int part = 0) {
   NearArgs NA;
   NA.p = c->p;
   NA.nsn = c->nsn;
@@ -379,6 +395,12 @@ static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K) {
   if (K) {
     if (stage) k_near<true, true><<<g, 128, nsm, s>>>(NA);
     else k_near<false, true><<<g, 128, nsm, s>>>(NA);
+  } else if (part == 1) {  // smooth-rule subtraction only (NEXT-4 mode)
+    if (stage) k_near<true, false, 1><<<g, 128, nsm, s>>>(NA);
+    else k_near<false, false, 1><<<g, 128, nsm, s>>>(NA);
+  } else if (part == 2) {  // exterior part only (measurement)
+    if (stage) k_near<true, false, 2><<<g, 128, nsm, s>>>(NA);
+    else k_near<false, false, 2><<<g, 128, nsm, s>>>(NA);
   } else {
     if (stage) k_near<true, false><<<g, 128, nsm, s>>>(NA);
     else k_near<false, false><<<g, 128, nsm, s>>>(NA);
@@ -419,12 +441,39 @@ static int run_near_off(bie_ctx* c, const double* tg, const double* tn, int64_t 
   return launch_check(c, tn ? "k_near_off<K>" : "k_near_off");
 }
 
+// NEXT-4 (PAPER §4.2): neighbours' exact fields re-expanded on each target
+// sphere through rotations (k_n4), accumulated in coefficient space.
+static int run_n4(bie_ctx* c, cudaStream_t s) {
+  const TableLayout L(c->p);
+  if (cudaMemsetAsync(c->d_psinear, 0, (size_t)c->ns * L.nlm * 6 * sizeof(double), s) != cudaSuccess)
+    return cuda_fail(c, cudaGetLastError(), "NEXT-4 psi reset");
+  if (c->n_near_tgt == 0) return BIE_OK;
+  N4Args NA;
+  NA.p = c->p;
+  NA.nsn = c->nsn;
+  NA.tab = c->d_tab;
+  NA.centres = c->d_centres;
+  NA.radii = c->d_radii;
+  NA.coef = c->d_ncoef;
+  NA.delta = c->d_delta;
+  NA.tgt = c->d_near_tgt;
+  NA.nb_off = c->d_nb_off;
+  NA.nb_idx = c->d_nb_idx;
+  NA.psi = c->d_psinear;
+  Ev ev;
+  prof_begin(c, BIE_KIND_NEAR4, s, &ev);
+  k_n4<<<(unsigned)c->n_near_tgt, 128, n4_smem_doubles(c->p) * sizeof(double), s>>>(NA);
+  prof_end(c, s, &ev);
+  return launch_check(c, "k_n4");
+}
+
 static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
                      cudaStream_t s) {
   // rows a2 + a4-a6: self term (or zeros) into u, packed sources into d_rec
   const bool near = (parts & BIE_PART_FAR) && c->n_near_tgt > 0;
-  const SelfArgs SA =
-      self_args(c, f, q, u, (parts & BIE_PART_SELF) ? 1 : 0, near ? c->d_alpha : nullptr, 0);
+  const bool n4 = near && (c->near_mode == 1 || c->near_mode == 3);
+  SelfArgs SA =
+      self_args(c, f, q, u, (parts & BIE_PART_SELF) && !n4 ? 1 : 0, near ? c->d_alpha : nullptr, 0);
   Ev ev;
   prof_begin(c, BIE_KIND_SELF, s, &ev);
   self_launch(c, SA, s);
@@ -436,10 +485,55 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
     rc = run_near_coef(c, s);
     if (rc) return rc;
   }
+  if (n4) {
+    // exact near fields as coefficients, then the self term's single inverse
+    // transform evaluates self + neighbours together
+    if ((rc = run_n4(c, s))) return rc;
+    SA = self_args(c, f, q, u, 1, nullptr, 0);
+    SA.psinear = c->d_psinear;
+    if (!(parts & BIE_PART_SELF)) SA.self = 2;  // far only: synthesise the neighbours' psi alone
+    prof_begin(c, BIE_KIND_SELF, s, &ev);
+    self_launch(c, SA, s);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_self(NEXT-4)"))) return rc;
+  }
   rc = run_far(c, u, s);
   if (rc || !near) return rc;
-  // NEXT-1: replace the smooth rule by the exterior expansion for near pairs
-  return run_near(c, u, s, false);
+  // NEXT-1: replace the smooth rule by the exterior expansion for near pairs;
+  // NEXT-4: subtract the smooth rule only (the exterior part is in u already)
+  const int part = c->near_mode == 0 ? 0 : (c->near_mode == 1 ? 1 : (c->near_mode == 2 ? 2 : -1));
+  if (part < 0) return BIE_OK;  // mode 3: NEXT-4 exterior part only (measurement)
+  return run_near(c, u, s, false, part);
+}
+
+// Launch a cluster-reduced far-field kernel: n_tt clusters of cl CTAs.
+template <class Kern>
+static cudaError_t launch_cluster(Kern kern, int n_tt, size_t smem, cudaStream_t s, const NbodyArgs& A,
+                                  int cl = kCL) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((int64_t)n_tt * cl));
+  cfg.blockDim = dim3(kTPB);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, A);
+}
+
+// The cluster size of the on-chip (DSMEM) chunk reduction, or 0 for HBM
+// partials + k_reduce: clusters only when selected (bie_set_far_reduction), the
+// launch leaves >= 16 units per resident slot and no chunk count is forced.
+// (Measured on cfg 5, profiles/r02_far_reduction.jsonl: see DESIGN.md §5.)
+static int cluster_size(const bie_ctx* c, const ChunkPlan& P, int occ, int64_t n_src_tiles, bool apply) {
+  if (c->chunks_override > 0 || c->far_red == 0) return 0;
+  const int cl = !apply ? kCL : (c->far_red == 2 ? 4 : (c->far_red == 3 ? 16 : kCL));
+  const int64_t slots = (int64_t)c->sm_count * std::max(occ, 1);
+  return (P.n_chunks > 1 && n_src_tiles >= 2 * cl && (int64_t)P.n_tt * cl >= 16 * slots) ? cl : 0;
 }
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
@@ -462,6 +556,22 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode) {
   A.pscale = 2.0 * c->mu;
   A.pout = nullptr;
   const size_t nb_smem = NbodySmem<kTS, kNST, false>::kBytes;
+  const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+  if (const int cl = cluster_size(c, P, mode ? c->occ_K : c->occ_apply, n_src_tiles, mode == 0)) {
+    A.n_chunks = cl;
+    A.tiles_per_chunk = (int)((n_src_tiles + cl - 1) / cl);
+    A.uinit = u;
+    A.uout = u;
+    prof_begin(c, kind, s, &ev);
+    const cudaError_t e =
+        mode ? launch_cluster(NBODY_K_CL, P.n_tt, nb_smem, s, A)
+             : (cl == 4 ? launch_cluster(NBODY_APPLY_CL4, P.n_tt, nb_smem, s, A, 4)
+                        : (cl == 16 ? launch_cluster(NBODY_APPLY_CL16, P.n_tt, nb_smem, s, A, 16)
+                                    : launch_cluster(NBODY_APPLY_CL, P.n_tt, nb_smem, s, A)));
+    prof_end(c, s, &ev);
+    if (e != cudaSuccess) return cuda_fail(c, e, "k_nbody (cluster)");
+    return launch_check(c, "k_nbody (cluster)");
+  }
   if (P.n_chunks == 1) {
     A.uinit = u;
     A.uout = u;
@@ -524,6 +634,19 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
     A.n_chunks = P.n_chunks;
     A.tiles_per_chunk = P.tiles_per_chunk;
     A.pscale = 2.0 * c->mu;
+    const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+    if (cluster_size(c, P, c->occ_off, n_src_tiles, false)) {
+      A.n_chunks = kCL;
+      A.tiles_per_chunk = (int)((n_src_tiles + kCL - 1) / kCL);
+      A.uout = u + 3 * b0;
+      A.pout = p ? p + b0 : nullptr;
+      prof_begin(c, BIE_KIND_OFFSURF, s, &ev);
+      const cudaError_t e = launch_cluster(NBODY_OFF_CL, P.n_tt, nb_smem, s, A);
+      prof_end(c, s, &ev);
+      if (e != cudaSuccess) return cuda_fail(c, e, "k_nbody_off (cluster)");
+      if ((rc = launch_check(c, "k_nbody_off (cluster)"))) return rc;
+      continue;
+    }
     if (P.n_chunks == 1) {
       A.uout = u + 3 * b0;
       A.pout = p ? p + b0 : nullptr;
@@ -596,6 +719,18 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
     A.n_chunks = P.n_chunks;
     A.tiles_per_chunk = P.tiles_per_chunk;
     A.pscale = 0.0;
+    const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+    if (cluster_size(c, P, c->occ_offK, n_src_tiles, false)) {
+      A.n_chunks = kCL;
+      A.tiles_per_chunk = (int)((n_src_tiles + kCL - 1) / kCL);
+      A.uout = t + 3 * b0;
+      prof_begin(c, BIE_KIND_KFAR, s, &ev);
+      const cudaError_t e = launch_cluster(NBODY_OFFK_CL, P.n_tt, nb_smem, s, A);
+      prof_end(c, s, &ev);
+      if (e != cudaSuccess) return cuda_fail(c, e, "k_nbody_offK (cluster)");
+      if ((rc = launch_check(c, "k_nbody_offK (cluster)"))) return rc;
+      continue;
+    }
     if (P.n_chunks == 1) {
       A.uout = t + 3 * b0;
       prof_begin(c, BIE_KIND_KFAR, s, &ev);
@@ -649,6 +784,8 @@ void bie_destroy(bie_ctx* c) {
     if (p) cudaFree(p);
   if (c->d_alpha) cudaFree(c->d_alpha);
   if (c->d_ncoef) cudaFree(c->d_ncoef);
+  if (c->d_delta) cudaFree(c->d_delta);
+  if (c->d_psinear) cudaFree(c->d_psinear);
   delete c;
 }
 
@@ -725,6 +862,10 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   prof_end(c, 0, &ev);
   set_self_smem(p);
   c->sht_occ = sht_prepare(p);
+  if (c->sht_occ < 1) {  // table layouts disagree or no kernel for this order
+    bie_destroy(c);
+    return BIE_ERR_UNSUPPORTED;
+  }
   // Dynamic shared memory opt-ins.  A staged near-correction variant whose
   // footprint exceeds the device limit is never launched (near_stage picks the
   // unstaged one), so it is skipped rather than requested.
@@ -740,11 +881,16 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   const size_t near_off = near_off_smem_doubles(p) * sizeof(double);
   smem((const void*)k_near<true, false>, near_st);
   smem((const void*)k_near<false, false>, near_un);
+  smem((const void*)k_near<true, false, 1>, near_st);
+  smem((const void*)k_near<false, false, 1>, near_un);
+  smem((const void*)k_near<true, false, 2>, near_st);
+  smem((const void*)k_near<false, false, 2>, near_un);
   smem((const void*)k_near<true, true>, near_st);
   smem((const void*)k_near<false, true>, near_un);
   smem((const void*)k_near_off<true, false>, near_off);
   smem((const void*)k_near_off<false, false>, near_off);
   smem((const void*)k_near_off<false, true>, near_off);
+  cudaFuncSetAttribute(NBODY_APPLY_CL16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
@@ -1086,6 +1232,48 @@ int bie_set_near(bie_ctx* c, double eta) {
 
 int64_t bie_near_pairs(const bie_ctx* c) { return c ? c->n_near_pairs : -1; }
 
+int bie_set_near_mode(bie_ctx* c, int mode) {
+  if (!c) return BIE_ERR_ARG;
+  int rc = check_device(c);
+  if (rc) return rc;
+  if (mode < 0 || mode > 3) return fail(c, BIE_ERR_ARG, "near mode must be 0, 1, 2 or 3%s");
+  if ((mode == 1 || mode == 3) && !c->d_delta) {
+    // Delta_n by quadrature on this context's grid (exact for n <= p), once
+    const TableLayout L(c->p);
+    double *rot = nullptr, *rphi = nullptr;
+    if (cudaMalloc(&c->d_delta, n4_delta_doubles(c->p) * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c->d_psinear, (size_t)c->ns * L.nlm * 6 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&rot, (size_t)c->nsn * L.nlm * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&rphi, (size_t)c->nsn * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(rot);
+      cudaFree(rphi);
+      cudaFree(c->d_delta);
+      cudaFree(c->d_psinear);
+      c->d_delta = c->d_psinear = nullptr;
+      return fail(c, BIE_ERR_ALLOC, "NEXT-4 tables%s");
+    }
+    Ev ev;
+    prof_begin(c, BIE_KIND_SETUP, 0, &ev);
+    k_n4_rotpts<<<(c->nsn + 127) / 128, 128>>>(c->p, c->d_tab, rot, rphi);
+    k_n4_delta<<<c->p + 1, 256>>>(c->p, c->d_tab, rot, rphi, c->d_delta);
+    c->launches[BIE_KIND_SETUP] += 1;
+    prof_end(c, 0, &ev);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaFree(rot);
+    cudaFree(rphi);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bie_set_near_mode");
+    const size_t sm = n4_smem_doubles(c->p) * sizeof(double);
+    if (sm > 48 * 1024 &&
+        cudaFuncSetAttribute((const void*)k_n4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+      return cuda_fail(c, cudaGetLastError(), "k_n4 shared memory");
+  }
+  c->near_mode = mode;
+  return BIE_OK;
+}
+
 // ----------------------------------------------------------- NEXT-2 (GMRES)
 namespace {
 struct Krylov {
@@ -1295,6 +1483,13 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
   if (e != cudaSuccess) return cuda_fail(c, e, "bie_solve_porous");
   if (iters_out) *iters_out = it;
   if (resid_out) *resid_out = rel;
+  return BIE_OK;
+}
+
+int bie_set_far_reduction(bie_ctx* c, int mode) {
+  if (!c) return BIE_ERR_ARG;
+  if (mode < 0 || mode > 3) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..3%s");
+  c->far_red = mode;
   return BIE_OK;
 }
 

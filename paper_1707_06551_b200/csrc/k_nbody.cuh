@@ -16,6 +16,8 @@
 // select applied only in source tiles that overlap the CTA's own spheres.
 // Chunk partials are reduced in fixed order by k_reduce (deterministic).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace bie {
@@ -99,14 +101,19 @@ __device__ __forceinline__ void pair_K(const double2 s0, const double2 s1, const
 
 // MODE 0: S + D (rows a3, a7); MODE 1: traction operator K (apply, or off-surface
 // targets with normals A.tn when OFF).
-template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0>
+// CL > 1: the CL source chunks of one target tile form a thread-block cluster
+// (launched with cluster dims (CL,1,1); chunk = cluster rank) and their partial
+// sums are reduced on chip through distributed shared memory, in fixed rank
+// order (deterministic), by the cluster itself -- no partials in HBM and no
+// k_reduce launch.  CL = 1: chunk partials go to HBM for k_reduce.
+template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0, int CL = 1>
 __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   using SM = NbodySmem<TS, NST, OFF>;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + NST * SM::kStageBytes);
 
-  const int tt = blockIdx.x % A.n_tt;
-  const int chunk = blockIdx.x / A.n_tt;
+  const int tt = CL > 1 ? (int)(blockIdx.x / CL) : (int)(blockIdx.x % A.n_tt);
+  const int chunk = CL > 1 ? (int)(blockIdx.x % CL) : (int)(blockIdx.x / A.n_tt);
   const int64_t n_src_tiles = (A.N + TS - 1) / TS;
   const int64_t tile0 = (int64_t)chunk * A.tiles_per_chunk;
   int ntile = (int)min((int64_t)A.tiles_per_chunk, n_src_tiles - tile0);
@@ -216,6 +223,53 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   }
 
   // ---- epilogue
+  if constexpr (CL > 1) {
+    // partials -> own shared memory (the ring is free: the loop ended with a
+    // barrier), cluster barrier, then rank q reduces targets [q T/CL, (q+1) T/CL)
+    // of the tile over ranks 0..CL-1 in order, reading the peers' shared memory.
+    constexpr int T = TPB * R;
+    constexpr int NC = OFF ? 4 : 3;
+    static_assert(NC * T * 8 <= NST * SM::kStageBytes, "reduction buffer");
+    double* red = reinterpret_cast<double*>(smraw);  // [NC][T]
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int li = r * TPB + threadIdx.x;
+      red[li] = acc[r][0];
+      red[T + li] = acc[r][1];
+      red[2 * T + li] = acc[r][2];
+      if (OFF) red[3 * T + li] = pacc[r];
+    }
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int q = (int)cl.block_rank();
+    const int lo_t = q * T / CL, hi_t = (q + 1) * T / CL;
+    const int64_t base = (int64_t)tt * T;
+    for (int li = lo_t + threadIdx.x; li < hi_t; li += TPB) {
+      const int64_t i = base + li;
+      if (i >= A.M) break;
+      double sm3[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sm3[c] = 0.0;
+      for (int rk = 0; rk < CL; ++rk) {
+        const double* rr = cl.map_shared_rank(red, rk);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sm3[c] += rr[c * T + li];
+      }
+      double u0 = sm3[0], u1 = sm3[1], u2 = sm3[2];
+      if (A.uinit) {
+        u0 = A.uinit[3 * i] + u0;
+        u1 = A.uinit[3 * i + 1] + u1;
+        u2 = A.uinit[3 * i + 2] + u2;
+      }
+      A.uout[3 * i] = u0;
+      A.uout[3 * i + 1] = u1;
+      A.uout[3 * i + 2] = u2;
+      if (OFF && A.pout) A.pout[i] = A.pscale * sm3[NC - 1];
+    }
+    cl.sync();  // peers keep their shared memory until every rank has read it
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t i = tidx[r];

@@ -52,7 +52,10 @@ __device__ __forceinline__ void exterior_field(int p, const double* __restrict__
 // memory first (broadcast reads in the O(n_s^2) smooth-rule subtraction).
 // K = false: velocity of S + D (NEXT-1); K = true: traction of S with the
 // target normal (NEXT-3, exterior_traction and the K pair kernel).
-template <bool STAGE, bool K>
+// PART (velocity, K = false): 0 exterior - smooth (NEXT-1); 1 smooth only
+// (NEXT-4 mode: the exterior part arrives in coefficient space, k_n4); 2
+// exterior only (measurement of the direct evaluation's cost; not an operator).
+template <bool STAGE, bool K, int PART = 0>
 __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = A.p, nsn = A.nsn;
@@ -100,12 +103,14 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
           pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
         }
       } else {
-        exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
+        ex[0] = ex[1] = ex[2] = 0.0;
+        if (PART != 1) exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
         double pdummy = 0.0;
-        for (int k = 0; k < nsn; ++k) {
-          const double2* q2 = sr + k * (kRec / 2);
-          pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
-        }
+        if (PART != 2)
+          for (int k = 0; k < nsn; ++k) {
+            const double2* q2 = sr + k * (kRec / 2);
+            pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
+          }
       }
       du[3 * kk + 0] += ex[0] - acc[0];
       du[3 * kk + 1] += ex[1] - acc[1];

@@ -38,6 +38,8 @@ struct SelfArgs {
   int self;         // compute the self term (else write zeros)
   double* alpha;    // nullable: [ns][2][nlm][3][2] projections <F,Y e_r>, <F,G>, <F,X>
                     // of (a/mu) f and q, for the near-singular correction (k_near)
+  const double* psinear = nullptr;  // k_sht only: [ns][nlm][6] psi^{Y,G,X} added before the
+                                    // inverse transform (NEXT-4 delayed evaluation)
   int precond;      // 1: u = P^{-1} q with P = 1/2 I + S_self + D_self (f ignored):
                     //    eigenvalue 1/(1/2 + lamS a/mu + lamD) on every VSH mode of
                     //    degree <= p and 2 on the rest (NEXT-2 preconditioner)

@@ -53,9 +53,26 @@ __host__ __device__ constexpr int sht_sb(int) { return 1; }
 // with the whole CTA -- so one group's load or barrier latency overlaps the
 // others' work.
 __host__ __device__ constexpr int sht_wps(int p) { return p <= 8 ? 1 : (p <= 16 ? 2 : 4); }
-__host__ __device__ constexpr int sht_groups(int p) { return p <= 8 ? 2 : 1; }
+__host__ __device__ constexpr int sht_groups(int p) { return p <= 4 ? 16 : (p <= 7 ? 12 : (p == 8 ? 9 : 1)); }
+// p <= 8: the fragment-order tables (<= 44 KB) are staged in shared memory once
+// per CTA and shared by all its groups; above, they are read through L1/L2.
+__host__ __device__ constexpr bool sht_tab_smem(int p) { return p <= 8; }
 
 __host__ __device__ constexpr int64_t sht_max(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// doubles of the fragment-order tables of order p (== ShtTabLayout(p).total)
+__host__ __device__ constexpr int64_t sht_tab_doubles(int p) {
+  const int P1 = p + 1;
+  int64_t o = 32LL * (((P1 + 4) / 4) * ((P1 + 7) / 8) + ((p + 3) / 4) * ((P1 + 7) / 8) +
+                      ((P1 + 3) / 4) * ((P1 + 8) / 8) + ((p + 3) / 4) * ((p + 7) / 8)) +
+              4 * P1;
+  for (int m = 0; m <= p; ++m) {
+    const int n = P1 - m;
+    o += 32LL * (((P1 + 3) / 4) * ((n + 7) / 8) + ((P1 + 3) / 4) * ((2 * n + 7) / 8) +
+                 ((n + 3) / 4) * ((P1 + 7) / 8) + ((2 * n + 3) / 4) * ((P1 + 7) / 8));
+  }
+  return o;
+}
 
 // Shared-memory carve-up of k_sht for order p (doubles).  Two big regions,
 // each reused by the phases in turn (sizes are the max over their tenants):
@@ -65,7 +82,7 @@ __host__ __device__ constexpr int64_t sht_max(int64_t a, int64_t b) { return a >
 // eigenvalue factors, the (m, c) decode of the coefficient index).
 struct ShtDims {
   int p, P1, NP, SB, nlm, ldG, ldF, ldE, KY, KX, ADm;
-  int64_t sizeG, sizeF, offG, offF, group, offTrig, offDeg, offMC, total;  // group = doubles per group
+  int64_t sizeG, sizeF, offG, offF, group, offTrig, offDeg, offMC, offTab, total;  // group = doubles per group
   __host__ __device__ constexpr ShtDims(int p_)
       : p(p_), P1(p_ + 1), NP(2 * p_ + 2), SB(sht_sb(p_)), nlm((p_ + 1) * (p_ + 2) / 2),
         ldG(sht_ld(p_ + 2 + sht_rup(p_, 4))),  // [g0 gP1 S | D] + K padding of the sin GEMM
@@ -86,7 +103,8 @@ struct ShtDims {
         group(sht_rup((int)sizeG, 2) + sht_rup((int)sizeF, 2)),
         offTrig(sht_groups(p_) * (int64_t)(sht_rup((int)sizeG, 2) + sht_rup((int)sizeF, 2))),
         offDeg(offTrig + 2 * (2 * p_ + 2) + 3 * (p_ + 1)), offMC(offDeg + 8 * (p_ + 1)),
-        total(offMC + ((p_ + 1) * (p_ + 2) / 2 + 1) / 2 + 2) {}
+        offTab(sht_rup((int)(offMC + ((p_ + 1) * (p_ + 2) / 2 + 1) / 2 + 2), 2)),
+        total(offTab + (sht_tab_smem(p_) ? sht_tab_doubles(p_) : 0)) {}
 };
 
 // Fragment-order table layout (built once per context by k_sht_tables).
@@ -228,7 +246,7 @@ __device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, 
       double b[KMAX];
 #pragma unroll
       for (int ks = 0; ks < KMAX; ++ks)
-        if (ks < KS) b[ks] = __ldg(Bf + (nt * KS + ks) * 32 + lane);
+        if (ks < KS) b[ks] = Bf[(nt * KS + ks) * 32 + lane];
       const double* a0 = A + (mt0 * 8 + (lane >> 2)) * lda + a_k0 + (lane & 3);
       const double* a1 = a0 + 8 * lda;
       double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
@@ -254,7 +272,7 @@ __device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, 
         const double* bf = Bf + (nt * KS + ks) * 32;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const double b0 = __ldg(bf + cc * 4 + kk), b1 = __ldg(bf + (cc + 1) * 4 + kk);
+          const double b0 = bf[cc * 4 + kk], b1 = bf[(cc + 1) * 4 + kk];
           const double x0 = a0[ks * 4 + kk];
           c00 = fma(x0, b0, c00);
           c01 = fma(x0, b1, c01);
@@ -273,8 +291,8 @@ __device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, 
 
 // ------------------------------------------------------------ the kernel
 template <int P, int NWARP, bool MMA>
-__global__ void __launch_bounds__(NWARP * 32, P <= 8 ? 7 : 1)
-    k_sht(SelfArgs A, const double* __restrict__ sht) {
+__global__ void __launch_bounds__(NWARP * 32, 1)
+    k_sht(SelfArgs A, const double* __restrict__ sht_g) {
   constexpr ShtDims Dm(P);
   constexpr int P1 = P + 1, NP = 2 * P + 2, nsn = P1 * NP, SB = Dm.SB;
   constexpr int ldG = Dm.ldG, ldF = Dm.ldF, ldE = Dm.ldE;
@@ -319,6 +337,14 @@ __global__ void __launch_bounds__(NWARP * 32, P <= 8 ? 7 : 1)
   }
   for (int m = 0, c0 = 0; m <= P; c0 += P1 - m, ++m)
     for (int c = c0 + tid; c < c0 + P1 - m; c += nt) mcode[c] = (m << 16) | (c - c0);
+  const double* sht = sht_g;
+  if constexpr (sht_tab_smem(P)) {  // stage the transform tables once per CTA
+    static_assert(sht_tab_doubles(P) % 2 == 0, "table size");
+    double2* dst = reinterpret_cast<double2*>(sm + Dm.offTab);
+    const double2* src = reinterpret_cast<const double2*>(sht_g);
+    for (int e = tid; e < (int)(sht_tab_doubles(P) / 2); e += nt) dst[e] = src[e];
+    sht = sm + Dm.offTab;
+  }
   const double* cph = trig;
   const double* sph = trig + NP;
   const double* ctj = trig + 2 * NP;
@@ -446,8 +472,8 @@ __global__ void __launch_bounds__(NWARP * 32, P <= 8 ? 7 : 1)
       int64_t aoff = 0;
       for (int m = 0; m <= P; ++m) {
         const int n = P1 - m;
-        const int64_t oCY = (int64_t)__ldg(sht + TL.mtab + 4 * m);
-        const int64_t oCGX = (int64_t)__ldg(sht + TL.mtab + 4 * m + 1);
+        const int64_t oCY = (int64_t)sht[TL.mtab + 4 * m];
+        const int64_t oCGX = (int64_t)sht[TL.mtab + 4 * m + 1];
         double* aY = AL + aoff;
         double* aX = aY + 4 * SB * n;
         const double* Fm = FT + m * 12 * SB * ldF;
@@ -542,6 +568,14 @@ __global__ void __launch_bounds__(NWARP * 32, P <= 8 ? 7 : 1)
         psi[2 + ri] = psV + psW;                      // psi^G (eq 2.16)
         psi[4 + ri] = psX;                            // psi^X
       }
+      if (A.self == 2)  // neighbours' coefficients alone (apply of the FAR part in NEXT-4 mode)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) psi[k] = 0.0;
+      if (A.psinear && b < nb) {  // NEXT-4: neighbours' coefficients
+        const double* pn = A.psinear + (s * nlm + lm_index(P, deg, m)) * 6;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) psi[k] += pn[k];
+      }
       double* Am = AD + m * ADm;
       double* Ay = Am;                 // [2 SB][KY]
       double* Ax = Am + 2 * SB * KY;   // [4 SB][KX]
@@ -579,8 +613,8 @@ __global__ void __launch_bounds__(NWARP * 32, P <= 8 ? 7 : 1)
       int item0 = 0;
       for (int m = 0; m <= P; ++m) {
         const int n = P1 - m;
-        const int64_t oDY = (int64_t)__ldg(sht + TL.mtab + 4 * m + 2);
-        const int64_t oDGX = (int64_t)__ldg(sht + TL.mtab + 4 * m + 3);
+        const int64_t oDY = (int64_t)sht[TL.mtab + 4 * m + 2];
+        const int64_t oDGX = (int64_t)sht[TL.mtab + 4 * m + 3];
         const double* Am = AD + m * ADm;
         auto stY = [&](int row, int col, double v0, double v1) {  // row = (b, ri), col = j
           if (row >= 2 * SB) return;
@@ -694,6 +728,7 @@ inline void* sht_kernel(int p, int variant, size_t* smem) {
 // Opt in to the dynamic shared memory of both variants for order p; returns
 // the resident CTAs per SM of the DMMA variant (the grid is sized from it).
 inline int sht_prepare(int p) {
+  if (sht_tab_doubles(p) != ShtTabLayout(p).total) return 0;  // layouts must agree
   int occ = 1;
   for (int v = 1; v >= 0; --v) {
     size_t smem = 0;

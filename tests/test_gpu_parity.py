@@ -341,3 +341,37 @@ def test_nearly_touching_spheres_and_zero_density(bie, oracle_mod):
     assert e.value.status == bie.BIE_ERR_GEOMETRY
     z = np.zeros((N, 3))
     assert np.all(gpu_apply(bie, c, a, p, 1.0, z, z) == 0.0)
+
+
+def test_cluster_reduction_matches_hbm_partials(bie, oracle_mod):
+    """cfg 5 (980,000 nodes): the far-field kernels reduce their 8 source chunks
+    on chip through distributed shared memory (thread-block clusters) when the
+    launch is large; bie_set_far_reduction(ctx, 1) forces HBM partials +
+    k_reduce.  Apply, off-surface u/p and the K apply agree to fp64 summation
+    grouping, and each path is deterministic run to run."""
+    d, f, q = _cfg_inputs(oracle_mod, 5)
+    ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
+    F, Q = _dev(f), _dev(q)
+    N = F.shape[0]
+    tg = _dev(d["targets"][:600000])
+    out = {}
+    for mode in (1, 0, 1):
+        bie.bie_set_far_reduction(ctx, mode)
+        u = torch.empty((N, 3), dtype=torch.float64, device="cuda")
+        bie.bie_apply_SLDL(ctx, F, Q, u)
+        uo = torch.empty((tg.shape[0], 3), dtype=torch.float64, device="cuda")
+        po = torch.empty(tg.shape[0], dtype=torch.float64, device="cuda")
+        bie.bie_eval_offsurface(ctx, F, Q, tg, uo, po)
+        k = torch.empty_like(u)
+        bie.bie_apply_K(ctx, F, k, bie.BIE_PART_FAR | bie.BIE_PART_SELF)
+        torch.cuda.synchronize()
+        res = [x.cpu().numpy() for x in (u, uo, po, k)]
+        if mode in out:
+            assert all(np.array_equal(a, b) for a, b in zip(out[mode], res)), "not deterministic"
+        out[mode] = res
+    ctx.close()
+    for a, b, what in zip(out[0], out[1], ("apply", "offsurface u", "offsurface p", "K")):
+        rel, mx = _err(a, b)
+        assert rel <= 1e-13 and mx <= 1e-12, (what, rel, mx)
+    sub = d["subset"][:128]
+    _assert_parity(out[1][3][sub], oracle_mod.apply_K(d["centres"], d["radii"], d["p"], f, sub), "K cluster")

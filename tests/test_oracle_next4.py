@@ -208,3 +208,31 @@ def test_near4_correction_definition(oracle_mod):
     assert np.abs(du - (est - two)).max() <= 1e-12 * np.abs(est).max()
     sub2 = np.arange(2 * nsn, 3 * nsn)  # sphere 2 has no neighbour
     assert np.all(oracle_mod.near4(c, a, p, mu, f, q, eta, sub2) == 0.0)
+
+
+def test_vsh_evaluation_is_pole_safe(oracle_mod):
+    """The stage-(3) evaluator works at directions on (or rounded onto) the polar
+    axis -- at even p a target node lies exactly on an axis-aligned pair axis.
+    It equals SciPy's harmonics at generic directions and is continuous at the
+    poles."""
+    p = 7
+    rng = np.random.default_rng(40)
+    a = rng.standard_normal(((p + 1) ** 2, 3)) + 1j * rng.standard_normal(((p + 1) ** 2, 3))
+    d = rng.standard_normal((30, 3))
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    th, ph = H.angles(d)
+    ref = np.zeros((30, 3), complex)
+    for n in range(p + 1):
+        for m in range(-n, n + 1):
+            Z = H.vsh(n, m, th, ph)
+            for ch in range(3):
+                if n == 0 and ch:
+                    continue
+                ref += a[n * n + n + m, ch] * Z[ch]
+    assert np.abs(oracle_mod.vsh_expand(p, a, d) - ref.real).max() <= 1e-13 * np.abs(ref).max()
+    for zs in (1.0, -1.0):
+        pole = oracle_mod.vsh_expand(p, a, np.array([[0.0, 0.0, zs], [1e-17, 0.0, zs]]))
+        near = oracle_mod.vsh_expand(p, a, np.array([[1e-7, 0.0, zs], [0.0, -1e-7, zs]]))
+        assert np.all(np.isfinite(pole))
+        assert np.abs(pole[0] - pole[1]).max() <= 1e-14 * np.abs(pole).max()
+        assert np.abs(near - pole[0]).max() <= 1e-5 * np.abs(pole).max()
