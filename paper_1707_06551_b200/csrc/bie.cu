@@ -11,6 +11,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/bie.h"
 #include "common.cuh"
 #include "k_complete.cuh"
@@ -86,6 +88,14 @@ struct bie_ctx {
   int* d_near_tgt = nullptr;
   double* d_alpha = nullptr;
   double* d_ncoef = nullptr;
+  // sphere cell grid for the off-surface near search (bie_set_near)
+  int* d_cell_start = nullptr;
+  int* d_cell_items = nullptr;
+  double g0[3] = {0, 0, 0}, gh = 1.0;
+  int gn[3] = {1, 1, 1};
+  // Morton-sorted target order scratch (off-surface near correction)
+  void* d_sort = nullptr;
+  size_t sort_cap = 0;
   // NEXT-4 (bie_set_near_mode): 0 direct, 1 rotated (PAPER §4.2), 2/3 measurement
   int near_mode = 0;
   double* d_delta = nullptr;    // packed Delta_n (rotation operator of T = Rx(-pi/2))
@@ -430,6 +440,47 @@ static int run_near_off(bie_ctx* c, const double* tg, const double* tn, int64_t 
   NO.tn = tn;
   NO.u = u;
   NO.pres = tn ? nullptr : p;
+  NO.cell_start = c->d_cell_start;
+  NO.cell_items = c->d_cell_items;
+  NO.g0x = c->g0[0];
+  NO.g0y = c->g0[1];
+  NO.g0z = c->g0[2];
+  NO.gh = c->gh;
+  NO.gnx = c->gn[0];
+  NO.gny = c->gn[1];
+  NO.gnz = c->gn[2];
+  // process the targets in Morton order of their grid cell: neighbouring lanes
+  // then share near spheres (coefficients and records hit L1 instead of L2)
+  if (m <= (int64_t)INT32_MAX) {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const int*)nullptr, (int*)nullptr, (int)m, 0, 30, s);
+    const size_t need = 2 * m * sizeof(uint32_t) + 2 * m * sizeof(int) + tmp + 256;
+    if (need > c->sort_cap) {
+      cudaFree(c->d_sort);
+      c->d_sort = nullptr;
+      c->sort_cap = 0;
+      if (cudaMalloc(&c->d_sort, need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, BIE_ERR_ALLOC, "near target sort scratch%s");
+      }
+      c->sort_cap = need;
+    }
+    char* b = static_cast<char*>(c->d_sort);
+    uint32_t* k_in = reinterpret_cast<uint32_t*>(b);
+    uint32_t* k_out = k_in + m;
+    int* i_in = reinterpret_cast<int*>(k_out + m);
+    int* i_out = i_in + m;
+    void* tmpb = reinterpret_cast<void*>(((uintptr_t)(i_out + m) + 255) & ~(uintptr_t)255);
+    Ev ev0;
+    prof_begin(c, BIE_KIND_NEAR, s, &ev0);
+    k_morton<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, tg, c->g0[0], c->g0[1], c->g0[2], c->gh, k_in,
+                                                        i_in);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmpb, tmp, k_in, k_out, i_in, i_out, (int)m, 0, 30, s);
+    prof_end(c, s, &ev0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "near target sort");
+    NO.order = i_out;
+  }
   const size_t sm = near_off_smem_doubles(c->p) * sizeof(double);
   const unsigned g = (unsigned)((m + 127) / 128);
   Ev ev;
@@ -786,6 +837,9 @@ void bie_destroy(bie_ctx* c) {
   if (c->d_ncoef) cudaFree(c->d_ncoef);
   if (c->d_delta) cudaFree(c->d_delta);
   if (c->d_psinear) cudaFree(c->d_psinear);
+  cudaFree(c->d_cell_start);
+  cudaFree(c->d_cell_items);
+  cudaFree(c->d_sort);
   delete c;
 }
 
@@ -1166,6 +1220,9 @@ int bie_reset_profile(bie_ctx* c) {
 }
 
 static void near_free(bie_ctx* c) {
+  cudaFree(c->d_cell_start);
+  cudaFree(c->d_cell_items);
+  c->d_cell_start = c->d_cell_items = nullptr;
   cudaFree(c->d_nb_off);
   cudaFree(c->d_nb_idx);
   cudaFree(c->d_near_tgt);
@@ -1197,6 +1254,54 @@ int bie_set_near(bie_ctx* c, double eta) {
   std::vector<int64_t> off;
   std::vector<int> idx, tgt;
   near_lists_host(hc.data(), ha.data(), ns, eta, off, idx);
+  // off-surface search grid: a target x is near sphere s only if
+  // |x - c_s| < a_s (1 + 2 eta) <= a_max (1 + 2 eta) = cell size (padded)
+  {
+    double amax = 0, lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t i = 0; i < ns; ++i) {
+      amax = std::max(amax, ha[i]);
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = std::min(lo[d], hc[3 * i + d]);
+        hi[d] = std::max(hi[d], hc[3 * i + d]);
+      }
+    }
+    double h = amax * (1.0 + 2.0 * eta) * (1.0 + 1e-9);
+    auto dims = [&](double hh, int* n) {
+      int64_t tot = 1;
+      for (int d = 0; d < 3; ++d) {
+        n[d] = (int)std::min<double>(1 << 20, std::floor((hi[d] - lo[d]) / hh) + 1.0);
+        tot *= n[d];
+      }
+      return tot;
+    };
+    while (dims(h, c->gn) > 8 * ns + 4096) h *= 1.25;  // bounded grid for sparse geometries
+    c->gh = h;
+    for (int d = 0; d < 3; ++d) c->g0[d] = lo[d];
+    const int64_t ncell = (int64_t)c->gn[0] * c->gn[1] * c->gn[2];
+    std::vector<int> start(ncell + 1, 0), items(ns), cellof(ns);
+    for (int64_t i = 0; i < ns; ++i) {
+      int q[3];
+      for (int d = 0; d < 3; ++d)
+        q[d] = std::min(c->gn[d] - 1, std::max(0, (int)std::floor((hc[3 * i + d] - lo[d]) / h)));
+      cellof[i] = (q[2] * c->gn[1] + q[1]) * c->gn[0] + q[0];
+      start[cellof[i] + 1]++;
+    }
+    for (int64_t k = 0; k < ncell; ++k) start[k + 1] += start[k];
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    for (int64_t i = 0; i < ns; ++i) items[fill[cellof[i]]++] = (int)i;  // ascending per cell
+    if (cudaMalloc(&c->d_cell_start, (ncell + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&c->d_cell_items, ns * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      near_free(c);
+      return fail(c, BIE_ERR_ALLOC, "near search grid%s");
+    }
+    if (cudaMemcpy(c->d_cell_start, start.data(), (ncell + 1) * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_cell_items, items.data(), ns * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaError_t e = cudaGetLastError();
+      near_free(c);
+      return cuda_fail(c, e, "bie_set_near: grid");
+    }
+  }
   if (off[ns] > (int64_t)INT32_MAX)
     return fail(c, BIE_ERR_UNSUPPORTED, "bie_set_near: more than 2^31-1 near pairs%s");
   std::vector<int> off32(ns + 1);

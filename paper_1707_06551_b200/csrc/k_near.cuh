@@ -277,11 +277,41 @@ struct NearOffArgs {
   double* u;           // [M][3] accumulated
   double* pres;        // [M] accumulated, nullable
   const double* tn = nullptr;  // [M][3] target normals (traction, K = true)
+  const int* order = nullptr;  // [M] processing order (Morton-sorted target indices), or identity
+  // uniform cell grid of the sphere centres (built by bie_set_near): a target
+  // x and sphere s are near only if |x - c_s| < a_s (1 + 2 eta) <= h, so
+  // every near sphere lies in the 27 cells around x's cell
+  const int* cell_start = nullptr;  // [ncell + 1]
+  const int* cell_items = nullptr;  // [ns] sphere indices, ascending within a cell
+  double g0x = 0, g0y = 0, g0z = 0, gh = 1;  // grid origin and cell size
+  int gnx = 1, gny = 1, gnz = 1;
 };
 
 __host__ __device__ inline int64_t near_off_smem_doubles(int p) {
   const int nlm = (p + 1) * (p + 2) / 2;
-  return 3LL * nlm + 4LL * kSphTile;
+  return 3LL * nlm;
+}
+
+// 30-bit Morton key of a point's cell (10 bits per axis, clamped to the grid)
+__device__ __forceinline__ uint32_t morton_spread(uint32_t v) {
+  v &= 0x3FF;
+  v = (v | (v << 16)) & 0x030000FF;
+  v = (v | (v << 8)) & 0x0300F00F;
+  v = (v | (v << 4)) & 0x030C30C3;
+  v = (v | (v << 2)) & 0x09249249;
+  return v;
+}
+__global__ void k_morton(int64_t M, const double* __restrict__ tx, double g0x, double g0y, double g0z,
+                         double h, uint32_t* __restrict__ key, int* __restrict__ idx) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= M) return;
+  auto q = [&](double v, double o) {
+    const double c = floor((v - o) / h);
+    return (uint32_t)(c < 0 ? 0 : (c > 1023 ? 1023 : c));
+  };
+  key[t] = morton_spread(q(tx[3 * t], g0x)) | (morton_spread(q(tx[3 * t + 1], g0y)) << 1) |
+           (morton_spread(q(tx[3 * t + 2], g0z)) << 2);
+  idx[t] = (int)t;
 }
 
 // K = true: traction with the target normals A.tn (bie_eval_traction, NEXT-3).
@@ -292,11 +322,12 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
   const TableLayout L(p);
   const int nlm = L.nlm;
   double* rt = sm;                // rA, rB, rC
-  double* tile = sm + 3 * nlm;    // [kSphTile][4]: centre, radius
   for (int e = threadIdx.x; e < 3 * nlm; e += blockDim.x) rt[e] = A.tab[L.rA + e];
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool live = t < A.M;
-  const int64_t tc = live ? t : A.M - 1;
+  __syncthreads();
+  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = it < A.M;
+  const int64_t t = live ? (A.order ? (int64_t)A.order[it] : it) : A.M - 1;
+  const int64_t tc = t;
   const double x[3] = {A.tx[3 * tc], A.tx[3 * tc + 1], A.tx[3 * tc + 2]};
   double nv[3] = {0.0, 0.0, 0.0};
   if constexpr (K) {
@@ -337,28 +368,31 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
     }
     cnt = 0;
   };
-  for (int64_t s0 = 0; s0 < A.ns; s0 += kSphTile) {
-    const int nt = (int)min((int64_t)kSphTile, A.ns - s0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nt; e += blockDim.x) {
-      tile[4 * e] = A.centres[3 * (s0 + e)];
-      tile[4 * e + 1] = A.centres[3 * (s0 + e) + 1];
-      tile[4 * e + 2] = A.centres[3 * (s0 + e) + 2];
-      tile[4 * e + 3] = A.radii[s0 + e];
-    }
-    __syncthreads();
-    for (int e = 0; e < nt; ++e) {
-      const double dx = __dsub_rn(x[0], tile[4 * e]), dy = __dsub_rn(x[1], tile[4 * e + 1]),
-                   dz = __dsub_rn(x[2], tile[4 * e + 2]);
-      const double a = tile[4 * e + 3];
-      const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-      const double dsurf = __dsub_rn(r, a);
-      if (live && dsurf >= 0.0 && dsurf < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {  // exterior only
-        list[cnt++] = (int)(s0 + e);
-        if (cnt == kNearList) flush();
+  // candidates: the 27 cells around x's (clamped) cell; the exact test of eq 4.5
+  // (point-to-surface form) in the oracle's evaluation order decides
+  auto cell = [&](double v, double o, int n) {
+    const double c = floor((v - o) / A.gh);
+    return (int)(c < 0 ? 0 : (c > n - 1 ? n - 1 : c));
+  };
+  const int cx = cell(x[0], A.g0x, A.gnx), cy = cell(x[1], A.g0y, A.gny), cz = cell(x[2], A.g0z, A.gnz);
+  for (int iz = max(cz - 1, 0); iz <= min(cz + 1, A.gnz - 1); ++iz)
+    for (int iy = max(cy - 1, 0); iy <= min(cy + 1, A.gny - 1); ++iy)
+      for (int ix = max(cx - 1, 0); ix <= min(cx + 1, A.gnx - 1); ++ix) {
+        const int cid = (iz * A.gny + iy) * A.gnx + ix;
+        for (int q = A.cell_start[cid]; q < A.cell_start[cid + 1]; ++q) {
+          const int sidx = A.cell_items[q];
+          const double dx = __dsub_rn(x[0], A.centres[3 * sidx]), dy = __dsub_rn(x[1], A.centres[3 * sidx + 1]),
+                       dz = __dsub_rn(x[2], A.centres[3 * sidx + 2]);
+          const double a = A.radii[sidx];
+          const double r =
+              __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+          const double dsurf = __dsub_rn(r, a);
+          if (live && dsurf >= 0.0 && dsurf < __dmul_rn(A.eta, __dmul_rn(2.0, a))) {  // exterior only
+            list[cnt++] = sidx;
+            if (cnt == kNearList) flush();
+          }
+        }
       }
-    }
-  }
   flush();
   if (!live) return;
   A.u[3 * t] += du[0];
