@@ -301,25 +301,34 @@ int bie_set_near_mode(bie_ctx* ctx, int mode);
 
 /*
  * Measurement knob: which kernel computes the spectral self term (rows a2,
- * a4-a6).  0 (default): k_sht, the batched small dense contractions on the
- * FP64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA); 1: the same schedule
- * with DFMA micro-kernels (compiled for p in {4, 6, 8, 12}; other orders use
- * variant 0); 2: the round-1 one-CTA-per-sphere kernel.  All three compute the
- * same operator (parity-tested); they differ only in schedule and speed.
- * Returns BIE_ERR_ARG for any other value.
+ * a4-a6).  -1 (default): the fastest measured for the context's order (2 for
+ * p <= 16, 0 above).  0: k_sht, the separable transforms as
+ * small dense contractions on the FP64 tensor cores (mma.sync m8n8k4 f64,
+ * SASS DMMA), one sphere per warp group; 1: the same schedule with DFMA
+ * micro-kernels (compiled for p in {4, 6, 8, 12}; other orders use 0); 2: the
+ * one-CTA-per-sphere scalar kernel.  All compute the same operator
+ * (parity-tested); they differ only in schedule and speed.  NEXT-4's
+ * coefficient accumulation always runs on k_sht.  BIE_ERR_ARG otherwise.
  */
 int bie_set_self_kernel(bie_ctx* ctx, int variant);
 
 /*
- * Measurement knob: how the far-field kernels combine their source chunks.
- * 0 (default): chunk partials in HBM, summed by a fixed-order reduction
- * kernel.  1 / 2 / 3: when the launch is large enough (>= 16 units per
- * resident CTA slot), the source chunks of a target tile run as ONE
- * thread-block cluster of 8 / 4 / 16 CTAs (16: apply only, non-portable size)
- * and are summed on chip through distributed shared memory in fixed rank
- * order -- no partials in HBM, no reduction launch; smaller launches keep the
- * HBM path.  All are deterministic; they differ only in fp64 summation
- * grouping.  BIE_ERR_ARG outside 0..3.
+ * Measurement knob: the schedule of the far-field pair-sum kernels.
+ * 1 (default): source chunks chosen by a wave-aware planner, one CTA per
+ *   (target tile, chunk) dispatched by the hardware, chunk partials in HBM, a
+ *   fixed-order reduction kernel.
+ * 0: stream-K -- one persistent CTA per resident slot, each given an equal
+ *   contiguous range of (target tile, source tile) units; a target tile whose
+ *   units span several CTAs is finished by a fixed-order fix-up kernel from at
+ *   most 2 partial tiles per CTA (no chunk partials; measured slower: the
+ *   static split cannot absorb SM-to-SM speed differences).
+ * 2 / 3 / 4: when the launch is large enough (>= 16 units per resident slot),
+ *   the 8 / 4 / 16 source chunks of a target tile run as ONE thread-block
+ *   cluster (16: apply only, non-portable size) and are summed on chip through
+ *   distributed shared memory in fixed rank order; smaller launches use 1.
+ * bie_set_source_chunks > 0 forces schedule 1.  All schedules are
+ * deterministic; they differ only in fp64 summation grouping.  BIE_ERR_ARG
+ * outside 0..4.
  */
 int bie_set_far_reduction(bie_ctx* ctx, int mode);
 

@@ -277,13 +277,13 @@ def bie_set_source_chunks(ctx, chunks: int):
 
 
 def bie_set_self_kernel(ctx, variant: int):
-    """Self-term kernel: 0 batched DMMA contractions (default), 1 batched DFMA,
-    2 the round-1 one-CTA-per-sphere kernel (include/bie.h)."""
+    """Self-term kernel: -1 auto (default), 0 DMMA contractions (k_sht), 1 DFMA,
+    2 the one-CTA-per-sphere scalar kernel (include/bie.h)."""
     _check(ctx, _lib.bie_set_self_kernel(ctx.handle, int(variant)))
 
 
 def bie_set_far_reduction(ctx, mode: int):
-    """0: cluster (DSMEM) reduction of source chunks when large enough; 1: HBM partials + k_reduce."""
+    """Far-field schedule: 1 chunk partials + k_reduce (default), 0 stream-K, 2/3/4 clusters of 8/4/16."""
     _check(ctx, _lib.bie_set_far_reduction(ctx.handle, int(mode)))
 
 

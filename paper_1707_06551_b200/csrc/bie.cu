@@ -47,6 +47,11 @@ constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 constexpr int kCL = 8;
 #define NBODY_APPLY_CL k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, kCL>
 #define NBODY_APPLY_CL4 k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, 4>
+// stream-K persistent variants (the default schedule)
+#define NBODY_APPLY_SK k_nbody_sk<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0>
+#define NBODY_OFF_SK k_nbody_sk<kR_OFF, kTPB, kTS, kNST, true, 1, 2, 0>
+#define NBODY_K_SK k_nbody_sk<kR_K, kTPB, kTS, kNST, false, 1, 2, 1>
+#define NBODY_OFFK_SK k_nbody_sk<kR_OFFK, kTPB, kTS, kNST, true, 1, 2, 1>
 #define NBODY_APPLY_CL16 k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, 16>
 #define NBODY_OFF_CL k_nbody<kR_OFF, kTPB, kTS, kNST, true, 1, 2, 0, kCL>
 #define NBODY_K_CL k_nbody<kR_K, kTPB, kTS, kNST, false, 1, 2, 1, kCL>
@@ -76,9 +81,11 @@ struct bie_ctx {
   size_t part_cap = 0;  // doubles
   double* d_sht = nullptr;  // fragment-order transform tables of k_sht
   int sht_occ = 1;          // resident k_sht CTAs per SM
-  int self_variant = 0;     // 0 k_sht DMMA, 1 k_sht DFMA, 2 round-1 k_self_t
+  int self_variant = -1;    // -1 auto (fastest measured per order), 0 k_sht DMMA, 1 k_sht DFMA,
+                            // 2 round-1 k_self_t
   int chunks_override = 0;
-  int far_red = 0;  // bie_set_far_reduction: 0 HBM partials + k_reduce; 1/2/3 clusters of 8/4/16
+  int far_red = 1;  // bie_set_far_reduction: 0 stream-K, 1 chunks + k_reduce (default), 2/3/4 clusters
+  int occ_sk[4] = {1, 1, 1, 1};  // resident CTAs per SM of the stream-K kernels (apply, off, K, offK)
   // near-singular correction (NEXT-1)
   double eta = 0.0;
   int n_near_tgt = 0;
@@ -338,13 +345,15 @@ static int launch_check(bie_ctx* c, const char* what) {
 // contractions, default) or the round-1 per-sphere k_self_t (kept for
 // comparison; bie_set_self_kernel).
 static void self_launch(bie_ctx* c, const SelfArgs& SA, cudaStream_t s) {
-  if (c->self_variant == 2 && !SA.psinear) {
+  // auto: the per-sphere kernel below p = 17, the batched DMMA contractions
+  // above (profiles/r02_self_bench.jsonl)
+  const int variant = c->self_variant >= 0 ? c->self_variant : (c->p <= 16 ? 2 : 0);
+  if (variant == 2 && !SA.psinear) {
     launch_self(SA, s);
     return;
   }
   // (NEXT-4's coefficient accumulation exists only in k_sht)
-  const cudaError_t e = launch_sht(SA, c->d_sht, c->self_variant == 2 ? 0 : c->self_variant, c->sm_count,
-                                   c->sht_occ, s);
+  const cudaError_t e = launch_sht(SA, c->d_sht, variant == 2 ? 0 : variant, c->sm_count, c->sht_occ, s);
   (void)e;  // surfaced by the caller's launch_check (cudaGetLastError)
 }
 
@@ -581,10 +590,34 @@ static cudaError_t launch_cluster(Kern kern, int n_tt, size_t smem, cudaStream_t
 // launch leaves >= 16 units per resident slot and no chunk count is forced.
 // (Measured on cfg 5, profiles/r02_far_reduction.jsonl: see DESIGN.md §5.)
 static int cluster_size(const bie_ctx* c, const ChunkPlan& P, int occ, int64_t n_src_tiles, bool apply) {
-  if (c->chunks_override > 0 || c->far_red == 0) return 0;
-  const int cl = !apply ? kCL : (c->far_red == 2 ? 4 : (c->far_red == 3 ? 16 : kCL));
+  if (c->chunks_override > 0 || c->far_red < 2) return 0;
+  const int cl = !apply ? kCL : (c->far_red == 3 ? 4 : (c->far_red == 4 ? 16 : kCL));
   const int64_t slots = (int64_t)c->sm_count * std::max(occ, 1);
   return (P.n_chunks > 1 && n_src_tiles >= 2 * cl && (int64_t)P.n_tt * cl >= 16 * slots) ? cl : 0;
+}
+
+// Stream-K far field (default schedule; k_nbody_sk + k_sk_fixup): G = one
+// persistent CTA per resident slot, equal contiguous ranges of (target tile,
+// source tile) units.  `which`: 0 apply, 1 off-surface, 2 K, 3 off-surface K.
+template <class Kern, class Fix>
+static int run_sk(bie_ctx* c, Kern kern, Fix fix, int which, int r, int nc, NbodyArgs A, size_t smem,
+                  int kind, cudaStream_t s) {
+  SkArgs K;
+  K.A = A;
+  K.S = (A.N + kTS - 1) / kTS;
+  K.A.n_tt = (int)((A.M + (int64_t)r * kTPB - 1) / ((int64_t)r * kTPB));
+  K.T = (int64_t)K.A.n_tt * K.S;
+  K.G = std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sm_count * c->occ_sk[which], K.T));
+  int rc = ensure_part(c, (size_t)2 * K.G * nc * r * kTPB);
+  if (rc) return rc;
+  K.part = c->d_part;
+  Ev ev;
+  prof_begin(c, kind, s, &ev);
+  kern<<<(unsigned)K.G, kTPB, smem, s>>>(K);
+  if (K.G > 1) fix<<<(unsigned)(K.G - 1), 256, 0, s>>>(K);
+  prof_end(c, s, &ev);
+  c->launches[kind] += K.G > 1 ? 1 : 0;
+  return launch_check(c, "k_nbody_sk");
 }
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
@@ -608,6 +641,13 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode) {
   A.pout = nullptr;
   const size_t nb_smem = NbodySmem<kTS, kNST, false>::kBytes;
   const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+  if (c->far_red == 0 && c->chunks_override == 0) {
+    A.uinit = u;
+    A.uout = u;
+    return mode ? run_sk(c, NBODY_K_SK, k_sk_fixup<kR_K * kTPB, false>, 2, kR_K, 3, A, nb_smem, kind, s)
+                : run_sk(c, NBODY_APPLY_SK, k_sk_fixup<kR_APPLY * kTPB, false>, 0, kR_APPLY, 3, A, nb_smem,
+                         kind, s);
+  }
   if (const int cl = cluster_size(c, P, mode ? c->occ_K : c->occ_apply, n_src_tiles, mode == 0)) {
     A.n_chunks = cl;
     A.tiles_per_chunk = (int)((n_src_tiles + cl - 1) / cl);
@@ -686,6 +726,14 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
     A.tiles_per_chunk = P.tiles_per_chunk;
     A.pscale = 2.0 * c->mu;
     const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+    if (c->far_red == 0 && c->chunks_override == 0) {
+      A.uout = u + 3 * b0;
+      A.pout = p ? p + b0 : nullptr;
+      if ((rc = run_sk(c, NBODY_OFF_SK, k_sk_fixup<kR_OFF * kTPB, true>, 1, kR_OFF, 4, A, nb_smem,
+                       BIE_KIND_OFFSURF, s)))
+        return rc;
+      continue;
+    }
     if (cluster_size(c, P, c->occ_off, n_src_tiles, false)) {
       A.n_chunks = kCL;
       A.tiles_per_chunk = (int)((n_src_tiles + kCL - 1) / kCL);
@@ -771,6 +819,13 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
     A.tiles_per_chunk = P.tiles_per_chunk;
     A.pscale = 0.0;
     const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+    if (c->far_red == 0 && c->chunks_override == 0) {
+      A.uout = t + 3 * b0;
+      if ((rc = run_sk(c, NBODY_OFFK_SK, k_sk_fixup<kR_OFFK * kTPB, true>, 3, kR_OFFK, 4, A, nb_smem,
+                       BIE_KIND_KFAR, s)))
+        return rc;
+      continue;
+    }
     if (cluster_size(c, P, c->occ_offK, n_src_tiles, false)) {
       A.n_chunks = kCL;
       A.tiles_per_chunk = (int)((n_src_tiles + kCL - 1) / kCL);
@@ -945,6 +1000,14 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   smem((const void*)k_near_off<false, false>, near_off);
   smem((const void*)k_near_off<false, true>, near_off);
   cudaFuncSetAttribute(NBODY_APPLY_CL16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sk[0], NBODY_APPLY_SK, kTPB,
+                                                NbodySmem<kTS, kNST, false>::kBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sk[1], NBODY_OFF_SK, kTPB,
+                                                NbodySmem<kTS, kNST, true>::kBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sk[2], NBODY_K_SK, kTPB,
+                                                NbodySmem<kTS, kNST, false>::kBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sk[3], NBODY_OFFK_SK, kTPB,
+                                                NbodySmem<kTS, kNST, true>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply, NBODY_APPLY, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_off, NBODY_OFF, kTPB,
@@ -1593,14 +1656,14 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
 
 int bie_set_far_reduction(bie_ctx* c, int mode) {
   if (!c) return BIE_ERR_ARG;
-  if (mode < 0 || mode > 3) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..3%s");
+  if (mode < 0 || mode > 4) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..4%s");
   c->far_red = mode;
   return BIE_OK;
 }
 
 int bie_set_self_kernel(bie_ctx* c, int variant) {
   if (!c) return BIE_ERR_ARG;
-  if (variant < 0 || variant > 2) return fail(c, BIE_ERR_ARG, "self kernel variant must be 0, 1 or 2%s");
+  if (variant < -1 || variant > 2) return fail(c, BIE_ERR_ARG, "self kernel variant must be -1, 0, 1 or 2%s");
   c->self_variant = variant;
   return BIE_OK;
 }

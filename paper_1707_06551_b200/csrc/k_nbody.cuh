@@ -316,3 +316,214 @@ __global__ void k_reduce(int64_t Mb, int n_chunks, const double* __restrict__ pa
 }
 
 }  // namespace bie
+
+namespace bie {
+
+// ---------------------------------------------------------------- stream-K
+// Persistent far-field kernel (the default schedule): the work units
+// (target tile tt, source tile st), flattened tt-major (u = tt S + st, S source
+// tiles, T = n_tt S units), are split into G equal contiguous ranges, one per
+// resident CTA slot, so every CTA does the same amount of work (no idle last
+// wave).  A CTA walks its range as segments of one target tile each; a segment
+// that covers all S source tiles of its tile writes the result directly, the
+// (at most two) partial segments of a CTA -- its first and its last -- go to
+// the partial buffer, slot 2c (first) / 2c+1 (last), and k_sk_fixup sums the
+// partials of every split tile in CTA order (deterministic).  HBM traffic:
+// targets once, records through L2, <= 2G partial tiles.
+__host__ __device__ __forceinline__ int64_t sk_u0(int64_t c, int64_t T, int64_t G) { return c * T / G; }
+// CTA whose range contains unit u: the largest c with sk_u0(c) <= u
+__host__ __device__ __forceinline__ int64_t sk_owner(int64_t u, int64_t T, int64_t G) {
+  return ((u + 1) * G + T - 1) / T - 1;
+}
+
+struct SkArgs {
+  NbodyArgs A;
+  int64_t S, T, G;   // source tiles, units, CTAs
+  double* part;      // [2G][NC][TPB R] partial tiles
+};
+
+template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0>
+__global__ void __launch_bounds__(TPB, MINB) k_nbody_sk(const SkArgs K) {
+  using SM = NbodySmem<TS, NST, OFF>;
+  constexpr int T_TILE = TPB * R;
+  constexpr int NC = OFF ? 4 : 3;
+  const NbodyArgs& A = K.A;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + NST * SM::kStageBytes);
+  const int64_t c = blockIdx.x;
+  const int64_t u_begin = sk_u0(c, K.T, K.G), u_end = sk_u0(c + 1, K.T, K.G);
+  const int64_t tt_first = u_begin / K.S;
+  const uint64_t pol = l2_evict_last_policy();
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < NST; ++st) mbar_init(&bar[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t g = 0;  // ring position over all of this CTA's source tiles (stage, parity)
+  for (int64_t u = u_begin; u < u_end;) {
+    const int64_t tt = u / K.S;
+    const int64_t st0 = u - tt * K.S;
+    const int64_t st1 = min(K.S, st0 + (u_end - u));
+    const int ntile = (int)(st1 - st0);
+    // ---- targets of tile tt in registers
+    double xt[R][3], acc[R][3], pacc[R];
+    double nx[MODE == 1 ? R : 1][3];
+    int lo[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = tt * T_TILE + r * TPB + threadIdx.x;
+      const int64_t ic = i < A.M ? i : A.M - 1;
+      if (OFF) {
+        xt[r][0] = A.tx[3 * ic];
+        xt[r][1] = A.tx[3 * ic + 1];
+        xt[r][2] = A.tx[3 * ic + 2];
+        lo[r] = 0;
+        if (MODE == 1) {
+          nx[MODE == 1 ? r : 0][0] = A.tn[3 * ic];
+          nx[MODE == 1 ? r : 0][1] = A.tn[3 * ic + 1];
+          nx[MODE == 1 ? r : 0][2] = A.tn[3 * ic + 2];
+        }
+      } else {
+        xt[r][0] = A.rec[ic * kRec];
+        xt[r][1] = A.rec[ic * kRec + 1];
+        xt[r][2] = A.rec[ic * kRec + 2];
+        lo[r] = (int)((ic / A.nsn) * A.nsn);
+        if (MODE == 1) {
+          nx[MODE == 1 ? r : 0][0] = A.rec[ic * kRec + 3];
+          nx[MODE == 1 ? r : 0][1] = A.rec[ic * kRec + 4];
+          nx[MODE == 1 ? r : 0][2] = A.rec[ic * kRec + 5];
+        }
+      }
+      acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+      pacc[r] = 0.0;
+    }
+    const int64_t first = tt * T_TILE;
+    const int64_t last = min(first + T_TILE, A.M) - 1;
+    const int64_t cta_lo = (first / A.nsn) * A.nsn;
+    const int64_t cta_hi = (last / A.nsn + 1) * A.nsn;
+    auto issue = [&](int it) {
+      const int st = (int)((g + it) % NST);
+      const int64_t k0 = (st0 + it) * TS;
+      const int cnt = (int)min((int64_t)TS, A.N - k0);
+      unsigned char* base = smraw + st * SM::kStageBytes;
+      const uint32_t bytes = cnt * kRec * 8;
+      const uint32_t qbytes = (OFF && MODE == 0) ? ((cnt + 1) & ~1) * 8 : 0;
+      mbar_arrive_expect_tx(&bar[st], bytes + qbytes);
+      bulk_g2s_hint(base, A.rec + k0 * kRec, bytes, &bar[st], pol);
+      if (OFF && MODE == 0) bulk_g2s(base + SM::kRecBytes, A.qn3 + k0, qbytes, &bar[st]);
+    };
+    if (threadIdx.x == 0)
+      for (int it = 0; it < NST && it < ntile; ++it) issue(it);
+    for (int it = 0; it < ntile; ++it) {
+      const int st = (int)((g + it) % NST);
+      mbar_wait(&bar[st], (uint32_t)(((g + it) / NST) & 1));
+      const int64_t k0 = (st0 + it) * TS;
+      const int cnt = (int)min((int64_t)TS, A.N - k0);
+      const double2* srec = reinterpret_cast<const double2*>(smraw + st * SM::kStageBytes);
+      const double* sqn = reinterpret_cast<const double*>(smraw + st * SM::kStageBytes + SM::kRecBytes);
+      const bool masked = !OFF && (k0 < cta_hi) && (k0 + cnt > cta_lo);
+      if (!masked) {
+#pragma unroll(UNR)
+        for (int sidx = 0; sidx < cnt; ++sidx) {
+          const double2* sr = srec + sidx * (kRec / 2);
+          const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
+          const double qn = (OFF && MODE == 0) ? sqn[sidx] : 0.0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (MODE == 1)
+              pair_K<false>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], 0, 0, 1);
+            else
+              pair_acc<false, OFF>(s0, s1, s2, s3, s4, s5, qn, xt[r], acc[r], pacc[r], 0, 0, 1);
+          }
+        }
+      } else {
+        for (int sidx = 0; sidx < cnt; ++sidx) {
+          const double2* sr = srec + sidx * (kRec / 2);
+          const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
+          const int k = (int)(k0 + sidx);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (MODE == 1)
+              pair_K<true>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], k, lo[r], A.nsn);
+            else
+              pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], k, lo[r],
+                                    A.nsn);
+          }
+        }
+      }
+      __syncthreads();  // every thread is done with stage st
+      if (threadIdx.x == 0 && it + NST < ntile) issue(it + NST);
+    }
+    g += ntile;
+    // ---- epilogue of the segment
+    const bool complete = st0 == 0 && st1 == K.S;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int li = r * TPB + threadIdx.x;
+      const int64_t i = first + li;
+      if (complete) {
+        if (i >= A.M) continue;
+        double u0 = acc[r][0], u1 = acc[r][1], u2 = acc[r][2];
+        if (A.uinit) {
+          u0 = A.uinit[3 * i] + u0;
+          u1 = A.uinit[3 * i + 1] + u1;
+          u2 = A.uinit[3 * i + 2] + u2;
+        }
+        A.uout[3 * i] = u0;
+        A.uout[3 * i + 1] = u1;
+        A.uout[3 * i + 2] = u2;
+        if (OFF && A.pout) A.pout[i] = A.pscale * pacc[r];
+      } else {
+        const int64_t slot = 2 * c + (tt == tt_first ? 0 : 1);
+        double* P = K.part + slot * NC * T_TILE;
+        __stcs(P + li, acc[r][0]);
+        __stcs(P + T_TILE + li, acc[r][1]);
+        __stcs(P + 2 * T_TILE + li, acc[r][2]);
+        if (OFF) __stcs(P + 3 * T_TILE + li, pacc[r]);
+      }
+    }
+    u += ntile;
+  }
+}
+
+// Sum the partial segments of every split target tile in CTA order: block b
+// handles the tile containing boundary b+1 if that is the tile's first boundary.
+template <int T_TILE, bool OFF>
+__global__ void k_sk_fixup(const SkArgs K) {
+  constexpr int NC = OFF ? 4 : 3;
+  const NbodyArgs& A = K.A;
+  const int64_t cb = blockIdx.x + 1;  // boundary between CTA cb-1 and cb
+  const int64_t ub = sk_u0(cb, K.T, K.G);
+  if (ub >= K.T || ub % K.S == 0) return;
+  const int64_t tt = ub / K.S;
+  const int64_t c_lo = sk_owner(tt * K.S, K.T, K.G);
+  if (c_lo != cb - 1) return;  // an earlier boundary of this tile handles it
+  const int64_t c_hi = sk_owner((tt + 1) * K.S - 1, K.T, K.G);
+  for (int li = threadIdx.x; li < T_TILE; li += blockDim.x) {
+    const int64_t i = tt * T_TILE + li;
+    if (i >= A.M) break;
+    double s[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) s[q] = 0.0;
+    for (int64_t cc = c_lo; cc <= c_hi; ++cc) {
+      if (sk_u0(cc, K.T, K.G) == sk_u0(cc + 1, K.T, K.G)) continue;  // empty range (T < G)
+      const int64_t slot = 2 * cc + (sk_u0(cc, K.T, K.G) / K.S == tt ? 0 : 1);
+      const double* P = K.part + slot * NC * T_TILE;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) s[q] += P[q * T_TILE + li];
+    }
+    double u0 = s[0], u1 = s[1], u2 = s[2];
+    if (A.uinit) {
+      u0 = A.uinit[3 * i] + u0;
+      u1 = A.uinit[3 * i + 1] + u1;
+      u2 = A.uinit[3 * i + 2] + u2;
+    }
+    A.uout[3 * i] = u0;
+    A.uout[3 * i + 1] = u1;
+    A.uout[3 * i + 2] = u2;
+    if (OFF && A.pout) A.pout[i] = A.pscale * s[NC - 1];
+  }
+}
+
+}  // namespace bie

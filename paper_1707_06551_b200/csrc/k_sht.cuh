@@ -230,7 +230,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // MMA = false: the same tiles on DFMA (the lane computes its two outputs with
 // a K loop; the A row and B column are read from shared/L1 per k).
 template <bool MMA, int KMAX, class Store>
-__device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, int a_k0, int M,
+__device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, int a_k0, int M, int K,
                                          const double* __restrict__ Bf, int KS, int NT, Store store,
                                          int item0, int nwarps) {
   const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % nwarps;  // warp within the group
@@ -250,11 +250,14 @@ __device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, 
       const double* a0 = A + (mt0 * 8 + (lane >> 2)) * lda + a_k0 + (lane & 3);
       const double* a1 = a0 + 8 * lda;
       double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+      // columns >= K of A are never read (their value would multiply a zero B
+      // pad row, but stale shared memory may hold anything): masked to 0
 #pragma unroll
       for (int ks = 0; ks < KMAX; ++ks) {
         if (ks < KS) {
-          dmma884(c00, c01, a0[ks * 4], b[ks]);
-          if (two) dmma884(c10, c11, a1[ks * 4], b[ks]);
+          const bool kin = ks * 4 + (lane & 3) < K;
+          dmma884(c00, c01, kin ? a0[ks * 4] : 0.0, b[ks]);
+          if (two) dmma884(c10, c11, kin ? a1[ks * 4] : 0.0, b[ks]);
         }
       }
       const int col = nt * 8 + 2 * (lane & 3);
@@ -272,6 +275,7 @@ __device__ __forceinline__ void sht_gemm(const double* __restrict__ A, int lda, 
         const double* bf = Bf + (nt * KS + ks) * 32;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
+          if (ks * 4 + kk >= K) break;
           const double b0 = bf[cc * 4 + kk], b1 = bf[(cc + 1) * 4 + kk];
           const double x0 = a0[ks * 4 + kk];
           c00 = fma(x0, b0, c00);
@@ -421,15 +425,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
           row[1 + k] = g1[d] + g2[d];   // S_k
           row[P1 + k] = g1[d] - g2[d];  // D_k
         }
-        if (k == 0)
-          for (int c = NP; c < ldG; ++c) row[c] = 0.0;  // K pad of the sin GEMM
       }
-    }
-    // K pad columns of the C-GEMM A operand (FT holds the previous batch's E output)
-    constexpr int padF = ldF - P1 > 0 ? ldF - P1 : 1;  // ldF > P1 always (sht_ld)
-    for (int e = gt; e < 12 * SB * P1 * padF; e += GT) {
-      const int row = e / padF;
-      FT[row * ldF + P1 + (e - row * padF)] = 0.0;
     }
     if (!A.self && !A.alpha) {  // pack only (+ zero u)
       if (A.u)
@@ -460,8 +456,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
         if (col < P1) FT[(col * 12 * SB + fr) * ldF + j] = v0;
         if (col + 1 < P1) FT[((col + 1) * 12 * SB + fr) * ldF + j] = v1;
       };
-      sht_gemm<MMA, KMAX>(G, ldG, 0, M, sht + TL.Tc, TL.KSc, TL.NTc, st_re, 0, WPS);
-      sht_gemm<MMA, KMAX>(G, ldG, P1 + 1, M, sht + TL.Ts, TL.KSs, TL.NTs, st_im,
+      sht_gemm<MMA, KMAX>(G, ldG, 0, M, P1 + 1, sht + TL.Tc, TL.KSc, TL.NTc, st_re, 0, WPS);
+      sht_gemm<MMA, KMAX>(G, ldG, P1 + 1, M, P, sht + TL.Ts, TL.KSs, TL.NTs, st_im,
                           TL.NTc * ((M + 15) / 16), WPS);
     }
     gsync();
@@ -488,9 +484,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
           if (col + 1 < 2 * n) aX[row * 2 * n + col + 1] = v1;
         };
         const int NTy = (n + 7) / 8, NTx = (2 * n + 7) / 8, KSc = (P1 + 3) / 4;
-        sht_gemm<MMA, KMAX>(Fm, ldF, 0, 4 * SB, sht + oCY, KSc, NTy, stY, item0, WPS);
+        sht_gemm<MMA, KMAX>(Fm, ldF, 0, 4 * SB, P1, sht + oCY, KSc, NTy, stY, item0, WPS);
         item0 += NTy * ((4 * SB + 15) / 16);
-        sht_gemm<MMA, KMAX>(Fm + 4 * SB * ldF, ldF, 0, 8 * SB, sht + oCGX, KSc, NTx, stX, item0, WPS);
+        sht_gemm<MMA, KMAX>(Fm + 4 * SB * ldF, ldF, 0, 8 * SB, P1, sht + oCGX, KSc, NTx, stX, item0, WPS);
         item0 += NTx * ((8 * SB + 15) / 16);
         aoff += 20 * SB * n;
       }
@@ -597,15 +593,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       gsync();
       continue;
     }
-    // K pads of the D-GEMM A blocks: columns n..KY-1 (Y rows), 2n..KX-1 (GX rows)
-    for (int e = gt; e < P1 * 6 * SB; e += GT) {
-      const int m = e / (6 * SB), row = e - m * 6 * SB, n = P1 - m;
-      double* Am = AD + m * ADm;
-      if (row < 2 * SB)
-        for (int c = n; c < sht_rup(n, 4); ++c) Am[row * KY + c] = 0.0;
-      else
-        for (int c = 2 * n; c < sht_rup(2 * n, 4); ++c) Am[2 * SB * KY + (row - 2 * SB) * KX + c] = 0.0;
-    }
     gsync();
     // ------------------------------------------------------------ D
     // U rows (b, comp, j): [Re U_0..p | Im U_0..p]
@@ -629,16 +616,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
           if (col + 1 < P1) U[((b * 3 + comp) * P1 + col + 1) * ldG + ri * P1 + m] = v1;
         };
         const int NTj = (P1 + 7) / 8;
-        sht_gemm<MMA, KMAX>(Am, KY, 0, 2 * SB, sht + oDY, (n + 3) / 4, NTj, stY, item0, WPS);
+        sht_gemm<MMA, KMAX>(Am, KY, 0, 2 * SB, n, sht + oDY, (n + 3) / 4, NTj, stY, item0, WPS);
         item0 += NTj * ((2 * SB + 15) / 16);
-        sht_gemm<MMA, KMAX>(Am + 2 * SB * KY, KX, 0, 4 * SB, sht + oDGX, (2 * n + 3) / 4, NTj, stX,
+        sht_gemm<MMA, KMAX>(Am + 2 * SB * KY, KX, 0, 4 * SB, 2 * n, sht + oDGX, (2 * n + 3) / 4, NTj, stX,
                             item0, WPS);
         item0 += NTj * ((4 * SB + 15) / 16);
-      }
-      // K pads of the E-GEMM A operand (columns 2 P1 .. ldG-1 of every U row)
-      for (int e = gt; e < 3 * P1 * SB * (ldG - NP); e += GT) {
-        const int row = e / (ldG - NP);
-        U[row * ldG + NP + (e - row * (ldG - NP))] = 0.0;
       }
     }
     gsync();
@@ -655,8 +637,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
         if (col < P) EO[row * ldE + P1 + 1 + col] = v0;
         if (col + 1 < P) EO[row * ldE + P1 + 2 + col] = v1;
       };
-      sht_gemm<MMA, KMAX>(U, ldG, 0, M, sht + TL.Ec, TL.KEc, TL.NEc, stc, 0, WPS);
-      sht_gemm<MMA, KMAX>(U, ldG, P1 + 1, M, sht + TL.Es, TL.KEs, TL.NEs, sts,
+      sht_gemm<MMA, KMAX>(U, ldG, 0, M, P1, sht + TL.Ec, TL.KEc, TL.NEc, stc, 0, WPS);
+      sht_gemm<MMA, KMAX>(U, ldG, P1 + 1, M, P, sht + TL.Es, TL.KEs, TL.NEs, sts,
                           TL.NEc * ((M + 15) / 16), WPS);
     }
     gsync();

@@ -343,19 +343,19 @@ def test_nearly_touching_spheres_and_zero_density(bie, oracle_mod):
     assert np.all(gpu_apply(bie, c, a, p, 1.0, z, z) == 0.0)
 
 
-def test_cluster_reduction_matches_hbm_partials(bie, oracle_mod):
-    """cfg 5 (980,000 nodes): the far-field kernels reduce their 8 source chunks
-    on chip through distributed shared memory (thread-block clusters) when the
-    launch is large; bie_set_far_reduction(ctx, 1) forces HBM partials +
-    k_reduce.  Apply, off-surface u/p and the K apply agree to fp64 summation
-    grouping, and each path is deterministic run to run."""
+def test_far_schedules_agree(bie, oracle_mod):
+    """cfg 5 (980,000 nodes): the far-field schedules (bie_set_far_reduction:
+    1 source chunks + HBM partials + k_reduce, the default; 0 stream-K
+    persistent CTAs + fix-up of split tiles; 2 clusters of 8 chunks reduced
+    through distributed shared memory) agree to fp64 summation grouping for the apply,
+    the off-surface u/p and the K apply, and each is deterministic run to run."""
     d, f, q = _cfg_inputs(oracle_mod, 5)
     ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
     F, Q = _dev(f), _dev(q)
     N = F.shape[0]
     tg = _dev(d["targets"][:600000])
     out = {}
-    for mode in (1, 0, 1):
+    for mode in (0, 1, 2, 0):
         bie.bie_set_far_reduction(ctx, mode)
         u = torch.empty((N, 3), dtype=torch.float64, device="cuda")
         bie.bie_apply_SLDL(ctx, F, Q, u)
@@ -370,8 +370,35 @@ def test_cluster_reduction_matches_hbm_partials(bie, oracle_mod):
             assert all(np.array_equal(a, b) for a, b in zip(out[mode], res)), "not deterministic"
         out[mode] = res
     ctx.close()
-    for a, b, what in zip(out[0], out[1], ("apply", "offsurface u", "offsurface p", "K")):
-        rel, mx = _err(a, b)
-        assert rel <= 1e-13 and mx <= 1e-12, (what, rel, mx)
+    for m in (1, 2):
+        for a, b, what in zip(out[0], out[m], ("apply", "offsurface u", "offsurface p", "K")):
+            rel, mx = _err(a, b)
+            assert rel <= 1e-13 and mx <= 1e-12, (m, what, rel, mx)
     sub = d["subset"][:128]
-    _assert_parity(out[1][3][sub], oracle_mod.apply_K(d["centres"], d["radii"], d["p"], f, sub), "K cluster")
+    _assert_parity(out[0][3][sub], oracle_mod.apply_K(d["centres"], d["radii"], d["p"], f, sub), "K stream-K")
+
+
+@pytest.mark.parametrize("ns,p", [(1, 3), (2, 1), (3, 4), (7, 6), (40, 5)])
+def test_stream_k_small_and_ragged(bie, oracle_mod, ns, p):
+    """Stream-K with fewer units than CTAs (empty ranges), tiles split across
+    many CTAs, and ragged last tiles: apply and off-surface vs the oracle."""
+    c, a, f, q, mu = _random_case(1300 + ns + p, ns, p, True, 1.2)
+    ctx = bie.bie_create(c, a, p, mu)
+    bie.bie_set_far_reduction(ctx, 0)
+    N = bie.bie_num_nodes(ctx)
+    ua = torch.empty((N, 3), dtype=torch.float64, device="cuda")
+    bie.bie_apply_SLDL(ctx, _dev(f), _dev(q), ua)
+    torch.cuda.synchronize()
+    _assert_parity(ua.cpu().numpy(), oracle_mod.apply(c, a, p, mu, f, q), f"sk apply {ns}")
+    rng = np.random.default_rng(ns)
+    tg = rng.uniform(-3, 3 + 4 * ns ** (1 / 3), (3001, 3))
+    dmin = np.min(np.linalg.norm(tg[:, None] - c[None], axis=-1) - a[None], axis=1)
+    tg = tg[np.abs(dmin) > 0.3]
+    uref, pref = oracle_mod.offsurface(c, a, p, mu, f, q, tg)
+    u = torch.empty((len(tg), 3), dtype=torch.float64, device="cuda")
+    pr = torch.empty(len(tg), dtype=torch.float64, device="cuda")
+    bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), _dev(tg), u, pr)
+    torch.cuda.synchronize()
+    ctx.close()
+    _assert_parity(u.cpu().numpy(), uref, "sk off u")
+    _assert_parity(pr.cpu().numpy(), pref, "sk off p")

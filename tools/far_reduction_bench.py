@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Far-field chunk reduction: HBM partials + k_reduce (mode 0) against on-chip
-thread-block-cluster reductions through distributed shared memory (modes 1/2/3
-= clusters of 8/4/16; bie_set_far_reduction).  Times bie_apply_SLDL's far
+"""Far-field schedules (bie_set_far_reduction): 0 stream-K persistent CTAs,
+1 source chunks + HBM partials + k_reduce (round 1), 2/3/4 on-chip
+thread-block-cluster reductions through distributed shared memory (clusters
+of 8/4/16).  Times bie_apply_SLDL's far
 field (kind nbody + reduce) and the off-surface evaluator on BASELINE configs,
 L2 flushed before every timed call.  Usage: python tools/far_reduction_bench.py [cfg ...]"""
 import json
@@ -29,7 +30,7 @@ def main():
         Q = torch.from_numpy(rng.standard_normal((N, 3))).cuda()
         U = torch.empty_like(F)
         tg = torch.from_numpy(d["targets"]).cuda() if d["targets"] is not None else None
-        for mode in (0, 1, 2, 3):
+        for mode in (0, 1, 2, 3, 4):
             bie.bie_set_far_reduction(ctx, mode)
             bie.bie_apply_SLDL(ctx, F, Q, U)
             torch.cuda.synchronize()

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--no-off", action="store_true")
     ap.add_argument("--targets", type=int, default=0, help="limit off-surface targets (0 = all)")
     ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--far-reduction", type=int, default=0, help="bie_set_far_reduction mode")
+    ap.add_argument("--self-kernel", type=int, default=0, help="bie_set_self_kernel variant")
     args = ap.parse_args()
     import torch
     import paper_1707_06551_b200 as bie
@@ -29,6 +31,8 @@ def main():
     ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
     if args.chunks:
         bie.bie_set_source_chunks(ctx, args.chunks)
+    bie.bie_set_far_reduction(ctx, args.far_reduction)
+    bie.bie_set_self_kernel(ctx, args.self_kernel)
     N = bie.bie_num_nodes(ctx)
     f_np, q_np = d["f"], d["q"]
     if d["rigid"] is not None:
