@@ -12,6 +12,7 @@
 // the correction runs after the far-field sum, one CTA per target sphere,
 // looping over its near neighbours in ascending index (deterministic).
 #pragma once
+#include <climits>
 #include "common.cuh"
 #include "k_nbody.cuh"
 #include "k_setup.cuh"
@@ -338,34 +339,34 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
   double du[3] = {0.0, 0.0, 0.0}, dp = 0.0;
   int list[kNearList];
   int cnt = 0;
-  auto flush = [&]() {
-    for (int j = 0; j < cnt; ++j) {
-      const int s = list[j];
-      const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
-      const double* cf = A.coef + (int64_t)s * nlm * 10;
-      const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
-      double ex[3], pe = 0.0, acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
-      if constexpr (K) {
-        exterior_traction(p, cf, rt, rt + nlm, cs, A.radii[s], x, nv, ex);
-        for (int k = 0; k < nsn; ++k) {
-          const double2* q2 = sr + k * (kRec / 2);
-          pair_K<false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 4), __ldg(q2 + 5), x, nv, acc, 0, 0, 1);
-        }
-      } else {
-        exterior_field<PRESSURE>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, A.radii[s], x, ex, &pe);
-        const double* sq = A.qn3 + (int64_t)s * nsn;
-        for (int k = 0; k < nsn; ++k) {
-          const double2* q2 = sr + k * (kRec / 2);
-          pair_acc<false, PRESSURE>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3),
-                                    __ldg(q2 + 4), __ldg(q2 + 5), PRESSURE ? __ldg(sq + k) : 0.0, x,
-                                    acc, pacc, 0, 0, 1);
-        }
+  auto eval = [&](int s) {
+    const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+    const double* cf = A.coef + (int64_t)s * nlm * 10;
+    const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
+    double ex[3], pe = 0.0, acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
+    if constexpr (K) {
+      exterior_traction(p, cf, rt, rt + nlm, cs, A.radii[s], x, nv, ex);
+      for (int k = 0; k < nsn; ++k) {
+        const double2* q2 = sr + k * (kRec / 2);
+        pair_K<false>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 4), __ldg(q2 + 5), x, nv, acc, 0, 0, 1);
       }
-      du[0] += ex[0] - acc[0];
-      du[1] += ex[1] - acc[1];
-      du[2] += ex[2] - acc[2];
-      if (PRESSURE) dp += pe - 2.0 * A.mu * pacc;
+    } else {
+      exterior_field<PRESSURE>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, A.radii[s], x, ex, &pe);
+      const double* sq = A.qn3 + (int64_t)s * nsn;
+      for (int k = 0; k < nsn; ++k) {
+        const double2* q2 = sr + k * (kRec / 2);
+        pair_acc<false, PRESSURE>(__ldg(q2), __ldg(q2 + 1), __ldg(q2 + 2), __ldg(q2 + 3),
+                                  __ldg(q2 + 4), __ldg(q2 + 5), PRESSURE ? __ldg(sq + k) : 0.0, x,
+                                  acc, pacc, 0, 0, 1);
+      }
     }
+    du[0] += ex[0] - acc[0];
+    du[1] += ex[1] - acc[1];
+    du[2] += ex[2] - acc[2];
+    if (PRESSURE) dp += pe - 2.0 * A.mu * pacc;
+  };
+  auto flush = [&]() {  // lane-local (a list overflow inside the scan)
+    for (int j = 0; j < cnt; ++j) eval(list[j]);
     cnt = 0;
   };
   // candidates: the 27 cells around x's (clamped) cell; the exact test of eq 4.5
@@ -393,7 +394,27 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
           }
         }
       }
-  flush();
+  // Final flush, warp-cooperative: every lane sorts its list; the warp walks
+  // the union in ascending sphere order and the lanes holding the current
+  // sphere evaluate it together, so its coefficients and records are read
+  // once per warp (broadcast) -- with Morton-ordered targets most lanes share
+  // most near spheres.  Per target the spheres still come in ascending order.
+  for (int i = 1; i < cnt; ++i) {
+    const int v = list[i];
+    int j = i - 1;
+    while (j >= 0 && list[j] > v) { list[j + 1] = list[j]; --j; }
+    list[j + 1] = v;
+  }
+  for (int head = 0;;) {
+    const int cand = head < cnt ? list[head] : INT_MAX;
+    const int smin = __reduce_min_sync(0xffffffffu, cand);
+    if (smin == INT_MAX) break;
+    if (cand == smin) {
+      eval(smin);
+      ++head;
+    }
+    __syncwarp();
+  }
   if (!live) return;
   A.u[3 * t] += du[0];
   A.u[3 * t + 1] += du[1];

@@ -52,7 +52,7 @@ __host__ __device__ constexpr int sht_sb(int) { return 1; }
 // independent -- they synchronise with named barriers (or __syncwarp), never
 // with the whole CTA -- so one group's load or barrier latency overlaps the
 // others' work.
-__host__ __device__ constexpr int sht_wps(int p) { return p <= 8 ? 1 : (p <= 16 ? 2 : 4); }
+__host__ __device__ constexpr int sht_wps(int p) { return p <= 8 ? 1 : (p <= 16 ? 2 : 8); }
 __host__ __device__ constexpr int sht_groups(int p) { return p <= 4 ? 16 : (p <= 7 ? 12 : (p == 8 ? 9 : 1)); }
 // p <= 8: the fragment-order tables (<= 44 KB) are staged in shared memory once
 // per CTA and shared by all its groups; above, they are read through L1/L2.
