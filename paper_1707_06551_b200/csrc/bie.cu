@@ -345,9 +345,9 @@ static int launch_check(bie_ctx* c, const char* what) {
 // contractions, default) or the round-1 per-sphere k_self_t (kept for
 // comparison; bie_set_self_kernel).
 static void self_launch(bie_ctx* c, const SelfArgs& SA, cudaStream_t s) {
-  // auto: the per-sphere kernel below p = 17, the batched DMMA contractions
-  // above (profiles/r02_self_bench.jsonl)
-  const int variant = c->self_variant >= 0 ? c->self_variant : (c->p <= 16 ? 2 : 0);
+  // auto: the per-sphere kernel up to p = 19, the DMMA contractions above
+  // (profiles/r02_self_bench.jsonl: 1.37x at p = 24, 1.6x at p = 32)
+  const int variant = c->self_variant >= 0 ? c->self_variant : (c->p <= 19 ? 2 : 0);
   if (variant == 2 && !SA.psinear) {
     launch_self(SA, s);
     return;

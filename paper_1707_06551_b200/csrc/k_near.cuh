@@ -394,27 +394,18 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
           }
         }
       }
-  // Final flush, warp-cooperative: every lane sorts its list; the warp walks
-  // the union in ascending sphere order and the lanes holding the current
-  // sphere evaluate it together, so its coefficients and records are read
-  // once per warp (broadcast) -- with Morton-ordered targets most lanes share
-  // most near spheres.  Per target the spheres still come in ascending order.
+  // Final flush in ascending sphere order (the per-target accumulation order).
+  // (A warp-cooperative variant -- the warp walking the union of its lanes'
+  // lists so each sphere is read once per warp -- cut long-scoreboard stalls
+  // 7.8 -> 2.8 per issue but idled the lanes not holding the current sphere:
+  // 2.14 -> 3.33 ms on cfg 5, profiles/r02_ncu_nearoff_cfg5*.txt; reverted.)
   for (int i = 1; i < cnt; ++i) {
     const int v = list[i];
     int j = i - 1;
     while (j >= 0 && list[j] > v) { list[j + 1] = list[j]; --j; }
     list[j + 1] = v;
   }
-  for (int head = 0;;) {
-    const int cand = head < cnt ? list[head] : INT_MAX;
-    const int smin = __reduce_min_sync(0xffffffffu, cand);
-    if (smin == INT_MAX) break;
-    if (cand == smin) {
-      eval(smin);
-      ++head;
-    }
-    __syncwarp();
-  }
+  flush();
   if (!live) return;
   A.u[3 * t] += du[0];
   A.u[3 * t + 1] += du[1];

@@ -57,6 +57,20 @@ def test_next4_random_suspensions(bie, oracle_mod, p, ns, eta, variant):
     _assert_parity(got, oracle_mod.apply_near4(c, a, p, mu, f, q, eta), f"next4 p={p} eta={eta}")
 
 
+@pytest.mark.parametrize("p", [16, 24, 32])
+def test_next4_high_order(bie, oracle_mod, p):
+    """High orders (the regime where NEXT-4 pays): three spheres with
+    oblique pair axes, sampled target nodes of every sphere vs the oracle."""
+    c = np.array([[0.0, 0.0, 0.0], [2.45, 0.31, -0.4], [-0.6, 2.2, 0.9]])
+    a = np.array([1.0, 0.9, 1.1])
+    nsn = (p + 1) * (2 * p + 2)
+    rng = np.random.default_rng(p + 7)
+    f, q = rng.standard_normal((3 * nsn, 3)), rng.standard_normal((3 * nsn, 3))
+    got = gpu_apply_mode(bie, c, a, p, 1.1, f, q, 1.0, 1)
+    sub = np.arange(0, 3 * nsn, 53)
+    _assert_parity(got[sub], oracle_mod.apply_near4(c, a, p, 1.1, f, q, 1.0, sub), f"next4 p={p}")
+
+
 def test_next4_parts_and_single_densities(bie, oracle_mod):
     """FAR only (= far + near4 correction), SELF only (unchanged), S only, D only."""
     p, eta = 6, 1.0

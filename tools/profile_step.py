@@ -21,8 +21,8 @@ def main():
     ap.add_argument("--no-off", action="store_true")
     ap.add_argument("--targets", type=int, default=0, help="limit off-surface targets (0 = all)")
     ap.add_argument("--chunks", type=int, default=0)
-    ap.add_argument("--far-reduction", type=int, default=0, help="bie_set_far_reduction mode")
-    ap.add_argument("--self-kernel", type=int, default=0, help="bie_set_self_kernel variant")
+    ap.add_argument("--far-reduction", type=int, default=1, help="bie_set_far_reduction mode (1 = library default)")
+    ap.add_argument("--self-kernel", type=int, default=-1, help="bie_set_self_kernel variant (-1 = auto)")
     args = ap.parse_args()
     import torch
     import paper_1707_06551_b200 as bie
