@@ -52,12 +52,12 @@ FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
 
 def _hbm_peak_gbps():
     """Measured HBM copy bandwidth from MEASURED_PEAKS.json (driver-written);
-    fallback: the same pool's measured 6451.5 GB/s."""
+    fallback when the file is absent: B200_PROFILING.md's 6650 GB/s."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return float(json.load(fh)["hbm_gbs"])
     except (OSError, KeyError, ValueError):
-        return 6451.5
+        return 6650.0
 
 
 HBM_PEAK_GBPS = _hbm_peak_gbps()

@@ -143,26 +143,6 @@ __device__ __forceinline__ Cx cfma_conj(Cx a, Cx b, Cx c) {  // conj(a) b + c
 }
 
 
-// x_out = sum_{m=-n..n} D[row(m)] v_m with v_{-m} = conj(v_m) (real-field
-// symmetry), v_m (m >= 0) at v[2 * vcol(m)]; D element index de(m); CONJ uses
-// conj(D).  Four independent accumulators keep four L2/L1 loads of D in
-// flight (the matrices of large p live in L2).
-template <bool CONJ, class VCol, class DE>
-__device__ __forceinline__ Cx n4_dot(const double* __restrict__ D, int n, const double* v, VCol vcol, DE de) {
-  Cx acc[4] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-  int k = 0;
-  for (int m = -n; m <= n; ++m, k = (k + 1) & 3) {
-    const int am = m < 0 ? -m : m;
-    const int cc = vcol(am);
-    Cx x = {v[2 * cc], v[2 * cc + 1]};
-    if (m < 0) x.i = -x.i;
-    const int e = de(m);
-    const Cx d = {__ldg(D + 2 * e), __ldg(D + 2 * e + 1)};
-    acc[k] = CONJ ? cfma_conj(d, x, acc[k]) : cfma(d, x, acc[k]);
-  }
-  return {(acc[0].r + acc[1].r) + (acc[2].r + acc[3].r), (acc[0].i + acc[1].i) + (acc[2].i + acc[3].i)};
-}
-
 // One CTA per target sphere with near neighbours; neighbours in ascending
 // index (deterministic accumulation).
 __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
@@ -215,10 +195,17 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
       const int f = e / nlm, c = e - f * nlm;
       const int2 nm = cofs(c);
       const int n = nm.x, mp = nm.y;
+      Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
       const int W = 2 * n + 1;
-      const Cx acc = n4_dot<false>(D, n, R1, [&](int am) { return f * nlm + lm_index(p, n, am); },
-                                   [&](int m) { return (mp + n) * W + (m + n); });
+      for (int m = -n; m <= n; ++m) {
+        const int am = m < 0 ? -m : m;
+        const int cc = f * nlm + lm_index(p, n, am);
+        Cx x = {R1[2 * cc], R1[2 * cc + 1]};
+        if (m < 0) x.i = -x.i;
+        const int de = (mp + n) * W + (m + n);
+        acc = cfma(Cx{__ldg(D + 2 * de), __ldg(D + 2 * de + 1)}, x, acc);
+      }
       double sb, cb;
       sincos(mp * beta, &sb, &cb);
       const Cx r = cmul(acc, Cx{cb, sb});
@@ -231,10 +218,17 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
       const int f = e / nlm, c = e - f * nlm;
       const int2 nm = cofs(c);
       const int n = nm.x, m = nm.y;
+      Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
       const int W = 2 * n + 1;
-      const Cx acc = n4_dot<true>(D, n, R2, [&](int amp) { return f * nlm + lm_index(p, n, amp); },
-                                  [&](int mp) { return (mp + n) * W + (m + n); });
+      for (int mp = -n; mp <= n; ++mp) {
+        const int amp = mp < 0 ? -mp : mp;
+        const int cc = f * nlm + lm_index(p, n, amp);
+        Cx x = {R2[2 * cc], R2[2 * cc + 1]};
+        if (mp < 0) x.i = -x.i;
+        const int de = (mp + n) * W + (m + n);
+        acc = cfma_conj(Cx{__ldg(D + 2 * de), __ldg(D + 2 * de + 1)}, x, acc);
+      }
       CR[8 * c + 2 * f] = acc.r;
       CR[8 * c + 2 * f + 1] = acc.i;
     }
@@ -335,10 +329,17 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
       const int f = e / nlm, c = e - f * nlm;
       const int2 nm = cofs(c);
       const int n = nm.x, mp = nm.y;
+      Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
       const int W = 2 * n + 1;
-      const Cx acc = n4_dot<false>(D, n, R1, [&](int am) { return f * nlm + lm_index(p, n, am); },
-                                   [&](int m) { return (mp + n) * W + (m + n); });
+      for (int m = -n; m <= n; ++m) {
+        const int am = m < 0 ? -m : m;
+        const int cc = f * nlm + lm_index(p, n, am);
+        Cx x = {R1[2 * cc], R1[2 * cc + 1]};
+        if (m < 0) x.i = -x.i;
+        const int de = (mp + n) * W + (m + n);
+        acc = cfma(Cx{__ldg(D + 2 * de), __ldg(D + 2 * de + 1)}, x, acc);
+      }
       double sb, cb;
       sincos(mp * beta, &sb, &cb);
       const Cx r = cmul(acc, Cx{cb, -sb});
@@ -351,10 +352,17 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
       const int f = e / nlm, c = e - f * nlm;
       const int2 nm = cofs(c);
       const int n = nm.x, m = nm.y;
+      Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
       const int W = 2 * n + 1;
-      const Cx acc = n4_dot<true>(D, n, R2, [&](int amp) { return f * nlm + lm_index(p, n, amp); },
-                                  [&](int mp) { return (mp + n) * W + (m + n); });
+      for (int mp = -n; mp <= n; ++mp) {
+        const int amp = mp < 0 ? -mp : mp;
+        const int cc = f * nlm + lm_index(p, n, amp);
+        Cx x = {R2[2 * cc], R2[2 * cc + 1]};
+        if (mp < 0) x.i = -x.i;
+        const int de = (mp + n) * W + (m + n);
+        acc = cfma_conj(Cx{__ldg(D + 2 * de), __ldg(D + 2 * de + 1)}, x, acc);
+      }
       double sa, ca;
       sincos(m * alpha, &sa, &ca);
       const Cx r = cmul(acc, Cx{ca, -sa});

@@ -321,6 +321,19 @@ def test_max_order_full_apply(bie, oracle_mod):
     c, a, f, q, mu = _random_case(1201, 2, p, True, 1.1)
     ref = oracle_mod.apply(c, a, p, mu, f, q)
     _assert_parity(gpu_apply(bie, c, a, p, mu, f, q), ref, "p=32 apply")
+    rng = np.random.default_rng(1202)
+    tg = rng.uniform(-4, 12, (4000, 3))
+    dmin = np.min(np.linalg.norm(tg[:, None] - c[None], axis=-1) - a[None], axis=1)
+    tg = tg[np.abs(dmin) > 0.2][:2000]
+    uref, pref = oracle_mod.offsurface(c, a, p, mu, f, q, tg)
+    ctx = bie.bie_create(c, a, p, mu)
+    u = torch.empty((len(tg), 3), dtype=torch.float64, device="cuda")
+    pr = torch.empty(len(tg), dtype=torch.float64, device="cuda")
+    bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), _dev(tg), u, pr)
+    torch.cuda.synchronize()
+    ctx.close()
+    _assert_parity(u.cpu().numpy(), uref, "p=32 offsurface u")
+    _assert_parity(pr.cpu().numpy(), pref, "p=32 offsurface p")
 
 
 def test_nearly_touching_spheres_and_zero_density(bie, oracle_mod):
