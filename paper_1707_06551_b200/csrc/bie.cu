@@ -40,6 +40,9 @@ constexpr int64_t kOffBatch = 1 << 21;  // off-surface targets per batch (bounds
 constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 
 #define NBODY_APPLY k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2>
+// near exclusion: the smooth rule skips eq-4.5 neighbour pairs (NEXT-1/4 on)
+#define NBODY_APPLY_NX k_nbody<kR_APPLY, kTPB, kTS, kNST, false, 1, 2, 0, 1, true>
+#define NBODY_K_NX k_nbody<kR_K, kTPB, kTS, kNST, false, 1, 2, 1, 1, true>
 #define NBODY_OFF k_nbody<kR_OFF, kTPB, kTS, kNST, true, 1, 2>
 #define NBODY_K k_nbody<kR_K, kTPB, kTS, kNST, false, 1, 2, 1>
 #define NBODY_OFFK k_nbody<kR_OFFK, kTPB, kTS, kNST, true, 1, 2, 1>
@@ -85,7 +88,8 @@ struct bie_ctx {
                             // 2 round-1 k_self_t
   int chunks_override = 0;
   int far_red = 1;  // bie_set_far_reduction: 0 stream-K, 1 chunks + k_reduce (default), 2/3/4 clusters
-  int occ_sk[4] = {1, 1, 1, 1};  // resident CTAs per SM of the stream-K kernels (apply, off, K, offK)
+  int occ_sk[4] = {1, 1, 1, 1};
+  int occ_apply_nx = 1, occ_K_nx = 1;  // resident CTAs per SM of the near-exclusion kernels  // resident CTAs per SM of the stream-K kernels (apply, off, K, offK)
   // near-singular correction (NEXT-1)
   double eta = 0.0;
   int n_near_tgt = 0;
@@ -377,7 +381,7 @@ static SelfArgs self_args(const bie_ctx* c, const double* f, const double* q, do
   return SA;
 }
 
-static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode = 0);
+static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode = 0, bool nx = false);
 
 // per-sphere exterior-expansion coefficients from the k_self projections
 static int run_near_coef(bie_ctx* c, cudaStream_t s) {
@@ -411,7 +415,10 @@ static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K, int part = 0)
   const bool stage = near_stage(c->p);
   const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
   const unsigned g = (unsigned)c->n_near_tgt;
-  if (K) {
+  if (K && part == 2) {  // exact traction only (the smooth K sum excluded these pairs)
+    if (stage) k_near<true, true, 2><<<g, 128, nsm, s>>>(NA);
+    else k_near<false, true, 2><<<g, 128, nsm, s>>>(NA);
+  } else if (K) {
     if (stage) k_near<true, true><<<g, 128, nsm, s>>>(NA);
     else k_near<false, true><<<g, 128, nsm, s>>>(NA);
   } else if (part == 1) {  // smooth-rule subtraction only (NEXT-4 mode)
@@ -557,13 +564,15 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_self(NEXT-4)"))) return rc;
   }
-  rc = run_far(c, u, s);
+  // near pairs: modes 0 and 1 exclude them from the smooth rule (k_nbody NX),
+  // so the correction only ADDS the exact exterior field -- NEXT-1: k_near's
+  // exterior part at the nodes; NEXT-4: nothing more (already in u through the
+  // self term's coefficients).  Modes 2/3 (measurement) keep the smooth rule.
+  const bool nx = near && (c->near_mode == 0 || c->near_mode == 1);
+  rc = run_far(c, u, s, 0, nx);
   if (rc || !near) return rc;
-  // NEXT-1: replace the smooth rule by the exterior expansion for near pairs;
-  // NEXT-4: subtract the smooth rule only (the exterior part is in u already)
-  const int part = c->near_mode == 0 ? 0 : (c->near_mode == 1 ? 1 : (c->near_mode == 2 ? 2 : -1));
-  if (part < 0) return BIE_OK;  // mode 3: NEXT-4 exterior part only (measurement)
-  return run_near(c, u, s, false, part);
+  if (c->near_mode == 1 || c->near_mode == 3) return BIE_OK;
+  return run_near(c, u, s, false, 2);
 }
 
 // Launch a cluster-reduced far-field kernel: n_tt clusters of cl CTAs.
@@ -621,11 +630,12 @@ static int run_sk(bie_ctx* c, Kern kern, Fix fix, int which, int r, int nc, Nbod
 }
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
-static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode) {
+static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode, bool nx) {
   Ev ev;
   int rc;
-  const ChunkPlan P =
-      plan_chunks(c, c->N, c->N, mode ? c->occ_K : c->occ_apply, mode ? kR_K : kR_APPLY);
+  const ChunkPlan P = plan_chunks(c, c->N, c->N,
+                                  mode ? (nx ? c->occ_K_nx : c->occ_K) : (nx ? c->occ_apply_nx : c->occ_apply),
+                                  mode ? kR_K : kR_APPLY);
   const int kind = mode ? BIE_KIND_KFAR : BIE_KIND_NBODY;
   NbodyArgs A;
   A.rec = c->d_rec;
@@ -641,6 +651,33 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode) {
   A.pout = nullptr;
   const size_t nb_smem = NbodySmem<kTS, kNST, false>::kBytes;
   const int64_t n_src_tiles = (c->N + kTS - 1) / kTS;
+  if (nx) {  // near exclusion (chunked schedule): neighbour pairs skipped by the smooth rule
+    A.nb_off = c->d_nb_off;
+    A.nb_idx = c->d_nb_idx;
+    const size_t sm_nx = nb_smem + kNxBytes;
+    if (P.n_chunks == 1) {
+      A.uinit = u;
+      A.uout = u;
+      prof_begin(c, kind, s, &ev);
+      if (mode) NBODY_K_NX<<<(unsigned)P.n_tt, kTPB, sm_nx, s>>>(A);
+      else NBODY_APPLY_NX<<<(unsigned)P.n_tt, kTPB, sm_nx, s>>>(A);
+      prof_end(c, s, &ev);
+      return launch_check(c, "k_nbody (near exclusion)");
+    }
+    if ((rc = ensure_part(c, (size_t)P.n_chunks * 3 * c->N))) return rc;
+    A.uinit = nullptr;
+    A.uout = c->d_part;
+    prof_begin(c, kind, s, &ev);
+    if (mode) NBODY_K_NX<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, sm_nx, s>>>(A);
+    else NBODY_APPLY_NX<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, sm_nx, s>>>(A);
+    prof_end(c, s, &ev);
+    if ((rc = launch_check(c, "k_nbody (near exclusion)"))) return rc;
+    prof_begin(c, BIE_KIND_REDUCE, s, &ev);
+    k_reduce<<<(unsigned)((3 * c->N + 255) / 256), 256, 0, s>>>(c->N, P.n_chunks, c->d_part, u, u, nullptr,
+                                                                 nullptr, 0.0);
+    prof_end(c, s, &ev);
+    return launch_check(c, "k_reduce");
+  }
   if (c->far_red == 0 && c->chunks_override == 0) {
     A.uinit = u;
     A.uout = u;
@@ -994,12 +1031,18 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   smem((const void*)k_near<false, false, 1>, near_un);
   smem((const void*)k_near<true, false, 2>, near_st);
   smem((const void*)k_near<false, false, 2>, near_un);
+  smem((const void*)k_near<true, true, 2>, near_st);
+  smem((const void*)k_near<false, true, 2>, near_un);
   smem((const void*)k_near<true, true>, near_st);
   smem((const void*)k_near<false, true>, near_un);
   smem((const void*)k_near_off<true, false>, near_off);
   smem((const void*)k_near_off<false, false>, near_off);
   smem((const void*)k_near_off<false, true>, near_off);
   cudaFuncSetAttribute(NBODY_APPLY_CL16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_apply_nx, NBODY_APPLY_NX, kTPB,
+                                                NbodySmem<kTS, kNST, false>::kBytes + kNxBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_K_nx, NBODY_K_NX, kTPB,
+                                                NbodySmem<kTS, kNST, false>::kBytes + kNxBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sk[0], NBODY_APPLY_SK, kTPB,
                                                 NbodySmem<kTS, kNST, false>::kBytes);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sk[1], NBODY_OFF_SK, kTPB,
@@ -1102,10 +1145,11 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
       rc = launch_check(c, "k_near_coef_K");
       if (rc) return rc;
     }
-    rc = run_far(c, u, s, 1);
+    // near pairs excluded from the smooth K sum; the exact traction is added
+    rc = run_far(c, u, s, 1, near);
     if (rc) return rc;
     if (near) {  // traction of the exact exterior expansion for near pairs
-      rc = run_near(c, u, s, true);
+      rc = run_near(c, u, s, true, 2);
       if (rc) return rc;
     }
   }

@@ -37,7 +37,28 @@ struct NbodyArgs {
   int tiles_per_chunk;  // source tiles per chunk
   double pscale;        // 2 mu (pressure)
   const double* tn = nullptr;  // [M][3] target normals (off-surface traction, OFF && MODE 1)
+  // NX (near exclusion, apply only): CSR eq-4.5 neighbour lists per sphere; the
+  // smooth rule skips the pairs of near spheres, whose exact field the near
+  // correction adds (so nothing has to be subtracted afterwards)
+  const int* nb_off = nullptr;
+  const int* nb_idx = nullptr;
 };
+
+// shared memory of the NX variant beyond the ring: the CTA's excluded-sphere
+// table -- (sphere, bitmask of the tile's target spheres that exclude it),
+// sorted by sphere -- staging for it, a count and one masked flag per stage
+constexpr int kNxCap = 768;  // >= 64 target spheres (p = 1) x 12 entries
+constexpr int kNxBytes = kNxCap * (4 + 8) * 2 + 32;
+
+// first index of the sorted table xs[0..n) with xs[i] >= v
+__device__ __forceinline__ int nx_lower(const int* xs, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (xs[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 
 template <int TS, int NST, bool OFF>
 struct NbodySmem {
@@ -106,11 +127,24 @@ __device__ __forceinline__ void pair_K(const double2 s0, const double2 s1, const
 // sums are reduced on chip through distributed shared memory, in fixed rank
 // order (deterministic), by the cluster itself -- no partials in HBM and no
 // k_reduce launch.  CL = 1: chunk partials go to HBM for k_reduce.
-template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0, int CL = 1>
+// NX (apply only, MODE 0, CL 1): pairs whose source sphere is the target's own
+// OR one of its eq-4.5 near neighbours are excluded from the smooth sum (the
+// near correction then adds only the exact exterior field).
+template <int R, int TPB, int TS, int NST, bool OFF, int MINB = 1, int UNR = 2, int MODE = 0, int CL = 1,
+          bool NX = false>
 __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   using SM = NbodySmem<TS, NST, OFF>;
+  static_assert(!NX || (!OFF && CL == 1), "near exclusion: apply kernels (S+D, K) only");
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + NST * SM::kStageBytes);
+  // NX tables (after the ring): sorted spheres xs, their target-sphere masks xm,
+  // unsorted staging (us, um), [0] count (-1: overflow), per-stage masked flags
+  uint64_t* xm = reinterpret_cast<uint64_t*>(smraw + SM::kBytes);
+  uint64_t* um = xm + kNxCap;
+  int* xs = reinterpret_cast<int*>(um + kNxCap);
+  int* us = xs + kNxCap;
+  int* xinfo = us + kNxCap;
+  unsigned char* mflag = reinterpret_cast<unsigned char*>(xinfo + 2);
 
   const int tt = CL > 1 ? (int)(blockIdx.x / CL) : (int)(blockIdx.x % A.n_tt);
   const int chunk = CL > 1 ? (int)(blockIdx.x % CL) : (int)(blockIdx.x / A.n_tt);
@@ -159,11 +193,49 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   const int64_t cta_lo = (first / A.nsn) * A.nsn;
   const int64_t cta_hi = (last / A.nsn + 1) * A.nsn;
 
+  const int t_lo = (int)(first / A.nsn);  // first target sphere of the tile
+  if constexpr (NX) {
+    // excluded-sphere table of the tile's targets (their own spheres and their
+    // eq-4.5 neighbours), each entry tagged with the bit of the target sphere
+    // that excludes it; rank-sorted by sphere (ties by position) by all threads
+    if (threadIdx.x == 0) {
+      int n = 0;
+      bool over = false;
+      for (int64_t t = t_lo; t <= last / A.nsn; ++t) {
+        const uint64_t bit = 1ull << (t - t_lo);
+        if (n < kNxCap) { us[n] = (int)t; um[n] = bit; ++n; } else over = true;
+        for (int q = A.nb_off[t]; q < A.nb_off[t + 1]; ++q) {
+          if (n < kNxCap) { us[n] = A.nb_idx[q]; um[n] = bit; ++n; } else over = true;
+        }
+      }
+      xinfo[0] = over ? -1 : n;
+    }
+    __syncthreads();
+    const int n = xinfo[0];
+    for (int i = threadIdx.x; i < n; i += TPB) {
+      const int v = us[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) rank += (us[j] < v) || (us[j] == v && j < i);
+      xs[rank] = v;
+      xm[rank] = um[i];
+    }
+    __syncthreads();
+  }
   const uint64_t pol = l2_evict_last_policy();  // records are re-read by every target tile
   auto issue = [&](int it) {
     const int st = it % NST;
     const int64_t k0 = (tile0 + it) * TS;
     const int cnt = (int)min((int64_t)TS, A.N - k0);
+    if constexpr (NX) {  // does the tile touch an excluded sphere?  (read after >= 1 barrier)
+      const int n = xinfo[0];
+      const int sa = (int)k0 / A.nsn, sb = ((int)k0 + cnt - 1) / A.nsn;
+      bool m = n < 0;
+      if (!m) {
+        const int i = nx_lower(xs, n, sa);
+        m = i < n && xs[i] <= sb;
+      }
+      mflag[st] = m ? 1 : 0;
+    }
     unsigned char* base = smraw + st * SM::kStageBytes;
     uint32_t bytes = cnt * kRec * 8;
     uint32_t qbytes = (OFF && MODE == 0) ? ((cnt + 1) & ~1) * 8 : 0;
@@ -180,6 +252,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   if (threadIdx.x == 0) {
     for (int it = 0; it < NST && it < ntile; ++it) issue(it);
   }
+  if constexpr (NX) __syncthreads();  // the first stages' masked flags
 
   for (int it = 0; it < ntile; ++it) {
     const int st = it % NST;
@@ -188,7 +261,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
     const int cnt = (int)min((int64_t)TS, A.N - k0);
     const double2* srec = reinterpret_cast<const double2*>(smraw + st * SM::kStageBytes);
     const double* sqn = reinterpret_cast<const double*>(smraw + st * SM::kStageBytes + SM::kRecBytes);
-    const bool masked = !OFF && (k0 < cta_hi) && (k0 + cnt > cta_lo);
+    const bool masked = NX ? mflag[st] != 0 : (!OFF && (k0 < cta_hi) && (k0 + cnt > cta_lo));
     if (!masked) {
 #pragma unroll(UNR)
       for (int sidx = 0; sidx < cnt; ++sidx) {
@@ -201,6 +274,44 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
             pair_K<false>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], 0, 0, 1);
           else
             pair_acc<false, OFF>(s0, s1, s2, s3, s4, s5, qn, xt[r], acc[r], pacc[r], 0, 0, 1);
+        }
+      }
+    } else if (NX) {
+      // per target: is the current source sphere its own or an eq-4.5
+      // neighbour?  (re-evaluated when the source sphere changes)
+      int scur = -1;
+      bool ex[R];
+      for (int sidx = 0; sidx < cnt; ++sidx) {
+        const int k = (int)(k0 + sidx);
+        const int sk = k / A.nsn;
+        if (sk != scur) {
+          scur = sk;
+          const int n = xinfo[0];
+          if (n >= 0) {  // target spheres excluding sk: OR of the table's masks
+            uint64_t mk = 0;
+            for (int i = nx_lower(xs, n, sk); i < n && xs[i] == sk; ++i) mk |= xm[i];
+#pragma unroll
+            for (int r = 0; r < R; ++r) ex[r] = (mk >> (lo[r] / A.nsn - t_lo)) & 1;
+          } else {  // table overflow: the neighbour lists themselves
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int tr = lo[r] / A.nsn;
+              bool e = tr == sk;
+              for (int q = A.nb_off[tr]; q < A.nb_off[tr + 1] && !e; ++q) e = A.nb_idx[q] == sk;
+              ex[r] = e;
+            }
+          }
+        }
+        const double2* sr = srec + sidx * (kRec / 2);
+        const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {  // (lo = k: masked; lo = k + nsn: not)
+          if (MODE == 1)
+            pair_K<true>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], k, ex[r] ? k : k + A.nsn,
+                         A.nsn);
+          else
+            pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], k,
+                                  ex[r] ? k : k + A.nsn, A.nsn);
         }
       }
     } else {

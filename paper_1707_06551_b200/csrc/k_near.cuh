@@ -99,10 +99,11 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
       if constexpr (K) {
         const double nx[3] = {ri[3], ri[4], ri[5]};
         exterior_traction(p, cf, rt, rt + nlm, cs, a, xt, nx, ex);
-        for (int k = 0; k < nsn; ++k) {
-          const double2* q2 = sr + k * (kRec / 2);
-          pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
-        }
+        if (PART != 2)
+          for (int k = 0; k < nsn; ++k) {
+            const double2* q2 = sr + k * (kRec / 2);
+            pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
+          }
       } else {
         ex[0] = ex[1] = ex[2] = 0.0;
         if (PART != 1) exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);

@@ -40,8 +40,9 @@ def main():
         prof = bie.bie_get_profile(ctx)
         near_ms = prof["near"][0] / reps
         # FP64 work per (target node, near source sphere): exterior expansion
-        # ~ 40 flops per (n, m) + smooth-rule subtraction 48 flops per source node
-        flops = npairs * nsn * (40.0 * nlm + 48.0 * nsn)
+        # ~ 40 flops per (n, m) (round 2: the smooth rule of near pairs is
+        # excluded inside the far-field kernel, nothing is subtracted)
+        flops = npairs * nsn * (40.0 * nlm)
         print(json.dumps({"config": cfg, "eta": eta, "p": p, "near_pairs": npairs,
                           "near_ms": near_ms, "apply_ms": sum(v[0] for v in prof.values()) / reps,
                           "nbody_ms": prof["nbody"][0] / reps,
