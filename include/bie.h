@@ -230,8 +230,12 @@ int bie_reset_profile(bie_ctx* ctx);
  * The same partition drives the traction paths (NEXT-3): bie_apply_K and
  * bie_eval_traction use the exact traction of the source expansion (eqs
  * 3.17-3.18) for near pairs / near exterior targets.
- * Builds the neighbour lists on the device and synchronises.  BIE_ERR_ARG for
- * eta < 0 or non-finite.
+ * In the applies (bie_apply_*, bie_apply_K) the far-field kernel skips the
+ * near pairs (as it skips a target's own sphere) and the correction adds the
+ * exact field, rather than adding it and subtracting the smooth rule.
+ * Builds the neighbour lists (host cell list, O(n_spheres); int64 offsets,
+ * BIE_ERR_UNSUPPORTED beyond 2^31 - 1 pairs) and the off-surface search grid,
+ * and synchronises.  BIE_ERR_ARG for eta < 0 or non-finite.
  */
 int bie_set_near(bie_ctx* ctx, double eta);
 
@@ -291,7 +295,8 @@ int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, i
  *     re-expansion of the exact near field on t (it differs from mode 0 by
  *     the degree > p tail of that field, which decays spectrally with p).
  *   2, 3: measurement only -- the exterior part alone (mode 0's and mode 1's
- *     respectively), without the smooth-rule subtraction; not an operator.
+ *     respectively) with the far field's smooth rule NOT excluding the near
+ *     pairs; not an operator.
  * Modes 1 and 3 build a (p+1)(2p+1)(2p+3)/3-entry complex table and an
  * [n_spheres][nlm][6] coefficient buffer on the first call (synchronous).
  * The traction operator and the off-surface evaluators always use mode 0.

@@ -47,8 +47,9 @@ struct NbodyArgs {
 // shared memory of the NX variant beyond the ring: the CTA's excluded-sphere
 // table -- (sphere, bitmask of the tile's target spheres that exclude it),
 // sorted by sphere -- staging for it, a count and one masked flag per stage
-constexpr int kNxCap = 768;  // >= 64 target spheres (p = 1) x 12 entries
-constexpr int kNxBytes = kNxCap * (4 + 8) * 2 + 32;
+constexpr int kNxCap = 256;     // table entries (overflow: per-pair neighbour-list lookups)
+constexpr int kNxTiles = 4096;  // masked-tile bitmap of the CTA's source range (else search)
+constexpr int kNxBytes = kNxCap * (4 + 8) * 2 + kNxTiles / 8 + 32;
 
 // first index of the sorted table xs[0..n) with xs[i] >= v
 __device__ __forceinline__ int nx_lower(const int* xs, int n, int v) {
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
   int* us = xs + kNxCap;
   int* xinfo = us + kNxCap;
   unsigned char* mflag = reinterpret_cast<unsigned char*>(xinfo + 2);
+  uint32_t* tbits = reinterpret_cast<uint32_t*>(xinfo + 4);  // masked tiles of [tile0, tile0 + ntile)
 
   const int tt = CL > 1 ? (int)(blockIdx.x / CL) : (int)(blockIdx.x % A.n_tt);
   const int chunk = CL > 1 ? (int)(blockIdx.x % CL) : (int)(blockIdx.x / A.n_tt);
@@ -219,6 +221,17 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
       xs[rank] = v;
       xm[rank] = um[i];
     }
+    // masked-tile bitmap of this CTA's source tiles (each thread one word)
+    if (ntile <= kNxTiles) {
+      for (int w = threadIdx.x; w < (ntile + 31) / 32; w += TPB) tbits[w] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += TPB) {  // tiles of excluded sphere xs[i]
+        const int64_t ta = (int64_t)xs[i] * A.nsn / TS - tile0;
+        const int64_t tb = ((int64_t)(xs[i] + 1) * A.nsn - 1) / TS - tile0;
+        for (int64_t t = max(ta, (int64_t)0); t <= min(tb, (int64_t)ntile - 1); ++t)
+          atomicOr(&tbits[t >> 5], 1u << (t & 31));
+      }
+    }
     __syncthreads();
   }
   const uint64_t pol = l2_evict_last_policy();  // records are re-read by every target tile
@@ -228,9 +241,11 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
     const int cnt = (int)min((int64_t)TS, A.N - k0);
     if constexpr (NX) {  // does the tile touch an excluded sphere?  (read after >= 1 barrier)
       const int n = xinfo[0];
-      const int sa = (int)k0 / A.nsn, sb = ((int)k0 + cnt - 1) / A.nsn;
       bool m = n < 0;
-      if (!m) {
+      if (!m && ntile <= kNxTiles) {
+        m = (tbits[it >> 5] >> (it & 31)) & 1u;
+      } else if (!m) {
+        const int sa = (int)k0 / A.nsn, sb = ((int)k0 + cnt - 1) / A.nsn;
         const int i = nx_lower(xs, n, sa);
         m = i < n && xs[i] <= sb;
       }
@@ -277,42 +292,72 @@ __global__ void __launch_bounds__(TPB, MINB) k_nbody(const NbodyArgs A) {
         }
       }
     } else if (NX) {
-      // per target: is the current source sphere its own or an eq-4.5
-      // neighbour?  (re-evaluated when the source sphere changes)
-      int scur = -1;
-      bool ex[R];
-      for (int sidx = 0; sidx < cnt; ++sidx) {
-        const int k = (int)(k0 + sidx);
+      // Segments of one source sphere each.  A sphere excluded by every target
+      // sphere of the tile is skipped, one excluded by none runs the unmasked
+      // unrolled loop, and only a mixed one takes the per-pair mask (targets
+      // of the same CTA on different spheres).
+      const int n = xinfo[0];
+      const int nts = (int)(last / A.nsn) - t_lo + 1;
+      const uint64_t all = nts >= 64 ? ~0ull : ((1ull << nts) - 1);
+      for (int seg = 0; seg < cnt;) {
+        const int k = (int)k0 + seg;
         const int sk = k / A.nsn;
-        if (sk != scur) {
-          scur = sk;
-          const int n = xinfo[0];
-          if (n >= 0) {  // target spheres excluding sk: OR of the table's masks
-            uint64_t mk = 0;
-            for (int i = nx_lower(xs, n, sk); i < n && xs[i] == sk; ++i) mk |= xm[i];
+        const int seg_end = min(cnt, (sk + 1) * A.nsn - (int)k0);
+        uint64_t mk = 0;
+        bool ex[R];
+        if (n >= 0) {  // target spheres excluding sk: OR of the table's masks
+          for (int i = nx_lower(xs, n, sk); i < n && xs[i] == sk; ++i) mk |= xm[i];
 #pragma unroll
-            for (int r = 0; r < R; ++r) ex[r] = (mk >> (lo[r] / A.nsn - t_lo)) & 1;
-          } else {  // table overflow: the neighbour lists themselves
+          for (int r = 0; r < R; ++r) ex[r] = (mk >> (lo[r] / A.nsn - t_lo)) & 1;
+        } else {  // table overflow: the neighbour lists themselves
+          mk = 1;  // (forces the per-pair path)
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int tr = lo[r] / A.nsn;
+            bool e = tr == sk;
+            for (int q = A.nb_off[tr]; q < A.nb_off[tr + 1] && !e; ++q) e = A.nb_idx[q] == sk;
+            ex[r] = e;
+          }
+        }
+        if (n >= 0 && (mk & all) == all) {
+          seg = seg_end;  // excluded for every target of the tile
+          continue;
+        }
+        if (mk == 0) {  // excluded for none: the unmasked loop
+#pragma unroll(UNR)
+          for (int sidx = seg; sidx < seg_end; ++sidx) {
+            const double2* sr = srec + sidx * (kRec / 2);
+            const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              const int tr = lo[r] / A.nsn;
-              bool e = tr == sk;
-              for (int q = A.nb_off[tr]; q < A.nb_off[tr + 1] && !e; ++q) e = A.nb_idx[q] == sk;
-              ex[r] = e;
+              if (MODE == 1)
+                pair_K<false>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], 0, 0, 1);
+              else
+                pair_acc<false, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], 0, 0, 1);
+            }
+          }
+        } else {
+          // mixed: per target, a node range that masks the whole segment
+          // (its sphere's start) or none (far below every index)
+          int lx[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) lx[r] = ex[r] ? sk * A.nsn : -(1 << 30);
+#pragma unroll(UNR)
+          for (int sidx = seg; sidx < seg_end; ++sidx) {
+            const int kk = (int)k0 + sidx;
+            const double2* sr = srec + sidx * (kRec / 2);
+            const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              if (MODE == 1)
+                pair_K<true>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], kk, lx[r], A.nsn);
+              else
+                pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], kk, lx[r],
+                                      A.nsn);
             }
           }
         }
-        const double2* sr = srec + sidx * (kRec / 2);
-        const double2 s0 = sr[0], s1 = sr[1], s2 = sr[2], s3 = sr[3], s4 = sr[4], s5 = sr[5];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {  // (lo = k: masked; lo = k + nsn: not)
-          if (MODE == 1)
-            pair_K<true>(s0, s1, s4, s5, xt[r], nx[MODE == 1 ? r : 0], acc[r], k, ex[r] ? k : k + A.nsn,
-                         A.nsn);
-          else
-            pair_acc<true, false>(s0, s1, s2, s3, s4, s5, 0.0, xt[r], acc[r], pacc[r], k,
-                                  ex[r] ? k : k + A.nsn, A.nsn);
-        }
+        seg = seg_end;
       }
     } else {
       for (int sidx = 0; sidx < cnt; ++sidx) {

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--far-reduction", type=int, default=1, help="bie_set_far_reduction mode (1 = library default)")
     ap.add_argument("--self-kernel", type=int, default=-1, help="bie_set_self_kernel variant (-1 = auto)")
+    ap.add_argument("--eta", type=float, default=0.0, help="bie_set_near (0 = off)")
+    ap.add_argument("--near-mode", type=int, default=0, help="bie_set_near_mode")
     args = ap.parse_args()
     import torch
     import paper_1707_06551_b200 as bie
@@ -33,6 +35,9 @@ def main():
         bie.bie_set_source_chunks(ctx, args.chunks)
     bie.bie_set_far_reduction(ctx, args.far_reduction)
     bie.bie_set_self_kernel(ctx, args.self_kernel)
+    if args.eta > 0:
+        bie.bie_set_near(ctx, args.eta)
+        bie.bie_set_near_mode(ctx, args.near_mode)
     N = bie.bie_num_nodes(ctx)
     f_np, q_np = d["f"], d["q"]
     if d["rigid"] is not None:
