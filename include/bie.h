@@ -230,9 +230,9 @@ int bie_reset_profile(bie_ctx* ctx);
  * The same partition drives the traction paths (NEXT-3): bie_apply_K and
  * bie_eval_traction use the exact traction of the source expansion (eqs
  * 3.17-3.18) for near pairs / near exterior targets.
- * In the applies (bie_apply_*, bie_apply_K) the far-field kernel skips the
- * near pairs (as it skips a target's own sphere) and the correction adds the
- * exact field, rather than adding it and subtracting the smooth rule.
+ * In the applies (bie_apply_*, bie_apply_K) the far-field kernel may skip the
+ * near pairs (as it skips a target's own sphere) so the correction only adds
+ * the exact field, or keep them and subtract them (bie_set_near_exclusion).
  * Builds the neighbour lists (host cell list, O(n_spheres); int64 offsets,
  * BIE_ERR_UNSUPPORTED beyond 2^31 - 1 pairs) and the off-surface search grid,
  * and synchronises.  BIE_ERR_ARG for eta < 0 or non-finite.
@@ -303,6 +303,16 @@ int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, i
  * Returns BIE_ERR_ARG for other modes.
  */
 int bie_set_near_mode(bie_ctx* ctx, int mode);
+
+/*
+ * How the applies treat the smooth rule of near pairs: 1 the far-field kernel
+ * skips them (the correction adds the exact field only); 0 the far field keeps
+ * them and the correction subtracts them pointwise; -1 (default) the cheaper
+ * by a cost model (skipping costs ~1.5 % of the far field, subtracting one
+ * smooth-rule pass per near pair).  Same operator either way (parity-tested);
+ * BIE_ERR_ARG outside -1..1.
+ */
+int bie_set_near_exclusion(bie_ctx* ctx, int mode);
 
 /*
  * Measurement knob: which kernel computes the spectral self term (rows a2,

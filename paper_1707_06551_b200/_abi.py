@@ -23,7 +23,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
-    "bie_set_self_kernel", "bie_set_near_mode", "bie_set_far_reduction",
+    "bie_set_self_kernel", "bie_set_near_mode", "bie_set_near_exclusion", "bie_set_far_reduction",
     "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K", "bie_eval_traction",
     "bie_status_string", "bie_last_error",
 )
@@ -57,6 +57,7 @@ _lib.bie_reset_profile.argtypes = [_vp]
 _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
 _lib.bie_set_self_kernel.argtypes = [_vp, _i32]
 _lib.bie_set_near_mode.argtypes = [_vp, _i32]
+_lib.bie_set_near_exclusion.argtypes = [_vp, _i32]
 _lib.bie_set_far_reduction.argtypes = [_vp, _i32]
 _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
@@ -285,6 +286,11 @@ def bie_set_self_kernel(ctx, variant: int):
 def bie_set_far_reduction(ctx, mode: int):
     """Far-field schedule: 1 chunk partials + k_reduce (default), 0 stream-K, 2/3/4 clusters of 8/4/16."""
     _check(ctx, _lib.bie_set_far_reduction(ctx.handle, int(mode)))
+
+
+def bie_set_near_exclusion(ctx, mode: int):
+    """Near pairs in the far field: 1 skipped, 0 subtracted, -1 auto (include/bie.h)."""
+    _check(ctx, _lib.bie_set_near_exclusion(ctx.handle, int(mode)))
 
 
 def bie_set_near_mode(ctx, mode: int):

@@ -109,7 +109,9 @@ struct bie_ctx {
   size_t sort_cap = 0;
   // NEXT-4 (bie_set_near_mode): 0 direct, 1 rotated (PAPER §4.2), 2/3 measurement
   int near_mode = 0;
+  int near_excl = -1;  // bie_set_near_exclusion: -1 auto (cost model), 0 subtract, 1 exclude
   double* d_delta = nullptr;    // packed Delta_n (rotation operator of T = Rx(-pi/2))
+  double* d_deltaT = nullptr;   // and its per-degree transpose
   double* d_psinear = nullptr;  // [ns][nlm][6] accumulated neighbour coefficients
   // staging for the _host entry points
   double *d_f = nullptr, *d_q = nullptr, *d_u = nullptr;
@@ -523,6 +525,7 @@ static int run_n4(bie_ctx* c, cudaStream_t s) {
   NA.radii = c->d_radii;
   NA.coef = c->d_ncoef;
   NA.delta = c->d_delta;
+  NA.deltaT = c->d_deltaT;
   NA.tgt = c->d_near_tgt;
   NA.nb_off = c->d_nb_off;
   NA.nb_idx = c->d_nb_idx;
@@ -532,6 +535,18 @@ static int run_n4(bie_ctx* c, cudaStream_t s) {
   k_n4<<<(unsigned)c->n_near_tgt, 128, n4_smem_doubles(c->p) * sizeof(double), s>>>(NA);
   prof_end(c, s, &ev);
   return launch_check(c, "k_n4");
+}
+
+// Near pairs in the far field: excluded inside k_nbody (NX; the correction then
+// only adds the exact field) or kept and subtracted by k_near.  Exclusion
+// costs ~1.5 % of the far field (masked-tile bookkeeping),
+// subtraction one smooth-rule pass per near pair at k_near's lower efficiency
+// (~3x per pair): auto picks the cheaper.
+static bool use_near_exclusion(const bie_ctx* c) {
+  if (c->near_excl >= 0) return c->near_excl == 1;
+  const double far_pairs = (double)c->N * (double)(c->N - c->nsn);
+  const double sub_pairs = (double)c->n_near_pairs * (double)c->nsn * (double)c->nsn;
+  return 0.015 * far_pairs < 3.0 * sub_pairs;
 }
 
 static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, int parts,
@@ -564,15 +579,18 @@ static int run_apply(bie_ctx* c, const double* f, const double* q, double* u, in
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_self(NEXT-4)"))) return rc;
   }
-  // near pairs: modes 0 and 1 exclude them from the smooth rule (k_nbody NX),
-  // so the correction only ADDS the exact exterior field -- NEXT-1: k_near's
-  // exterior part at the nodes; NEXT-4: nothing more (already in u through the
-  // self term's coefficients).  Modes 2/3 (measurement) keep the smooth rule.
-  const bool nx = near && (c->near_mode == 0 || c->near_mode == 1);
+  // near pairs (modes 0, 1): excluded from the smooth rule (k_nbody NX) so the
+  // correction only ADDS the exact exterior field, or kept and subtracted by
+  // k_near (use_near_exclusion).  NEXT-1: k_near's exterior part (- smooth);
+  // NEXT-4: the exterior part is already in u through the self term's
+  // coefficients (k_near: - smooth only, when not excluded).  Modes 2/3
+  // (measurement): the exterior part alone, smooth rule kept.
+  const bool nx = near && (c->near_mode == 0 || c->near_mode == 1) && use_near_exclusion(c);
   rc = run_far(c, u, s, 0, nx);
   if (rc || !near) return rc;
-  if (c->near_mode == 1 || c->near_mode == 3) return BIE_OK;
-  return run_near(c, u, s, false, 2);
+  if (c->near_mode == 3 || (c->near_mode == 1 && nx)) return BIE_OK;
+  const int part = c->near_mode == 2 || nx ? 2 : (c->near_mode == 1 ? 1 : 0);
+  return run_near(c, u, s, false, part);
 }
 
 // Launch a cluster-reduced far-field kernel: n_tt clusters of cl CTAs.
@@ -928,6 +946,7 @@ void bie_destroy(bie_ctx* c) {
   if (c->d_alpha) cudaFree(c->d_alpha);
   if (c->d_ncoef) cudaFree(c->d_ncoef);
   if (c->d_delta) cudaFree(c->d_delta);
+  if (c->d_deltaT) cudaFree(c->d_deltaT);
   if (c->d_psinear) cudaFree(c->d_psinear);
   cudaFree(c->d_cell_start);
   cudaFree(c->d_cell_items);
@@ -1145,11 +1164,12 @@ int bie_apply_K(bie_ctx* c, const double* sigma, double* u, int parts, bie_strea
       rc = launch_check(c, "k_near_coef_K");
       if (rc) return rc;
     }
-    // near pairs excluded from the smooth K sum; the exact traction is added
-    rc = run_far(c, u, s, 1, near);
+    // near pairs excluded from the smooth K sum (or subtracted by k_near)
+    const bool nx = near && use_near_exclusion(c);
+    rc = run_far(c, u, s, 1, nx);
     if (rc) return rc;
     if (near) {  // traction of the exact exterior expansion for near pairs
-      rc = run_near(c, u, s, true, 2);
+      rc = run_near(c, u, s, true, nx ? 2 : 0);
       if (rc) return rc;
     }
   }
@@ -1444,6 +1464,13 @@ int bie_set_near(bie_ctx* c, double eta) {
 
 int64_t bie_near_pairs(const bie_ctx* c) { return c ? c->n_near_pairs : -1; }
 
+int bie_set_near_exclusion(bie_ctx* c, int mode) {
+  if (!c) return BIE_ERR_ARG;
+  if (mode < -1 || mode > 1) return fail(c, BIE_ERR_ARG, "near exclusion must be -1, 0 or 1%s");
+  c->near_excl = mode;
+  return BIE_OK;
+}
+
 int bie_set_near_mode(bie_ctx* c, int mode) {
   if (!c) return BIE_ERR_ARG;
   int rc = check_device(c);
@@ -1454,6 +1481,7 @@ int bie_set_near_mode(bie_ctx* c, int mode) {
     const TableLayout L(c->p);
     double *rot = nullptr, *rphi = nullptr;
     if (cudaMalloc(&c->d_delta, n4_delta_doubles(c->p) * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c->d_deltaT, n4_delta_doubles(c->p) * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&c->d_psinear, (size_t)c->ns * L.nlm * 6 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&rot, (size_t)c->nsn * L.nlm * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&rphi, (size_t)c->nsn * sizeof(double)) != cudaSuccess) {
@@ -1461,14 +1489,15 @@ int bie_set_near_mode(bie_ctx* c, int mode) {
       cudaFree(rot);
       cudaFree(rphi);
       cudaFree(c->d_delta);
+      cudaFree(c->d_deltaT);
       cudaFree(c->d_psinear);
-      c->d_delta = c->d_psinear = nullptr;
+      c->d_delta = c->d_deltaT = c->d_psinear = nullptr;
       return fail(c, BIE_ERR_ALLOC, "NEXT-4 tables%s");
     }
     Ev ev;
     prof_begin(c, BIE_KIND_SETUP, 0, &ev);
     k_n4_rotpts<<<(c->nsn + 127) / 128, 128>>>(c->p, c->d_tab, rot, rphi);
-    k_n4_delta<<<c->p + 1, 256>>>(c->p, c->d_tab, rot, rphi, c->d_delta);
+    k_n4_delta<<<c->p + 1, 256>>>(c->p, c->d_tab, rot, rphi, c->d_delta, c->d_deltaT);
     c->launches[BIE_KIND_SETUP] += 1;
     prof_end(c, 0, &ev);
     cudaError_t e = cudaDeviceSynchronize();

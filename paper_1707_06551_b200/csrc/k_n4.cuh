@@ -85,7 +85,8 @@ __global__ void k_n4_rotpts(int p, const double* __restrict__ tab, double* __res
 // Setup 2: Delta_n[m'][m] = <Y_n^m', Y_n^m o T> by the grid quadrature (exact:
 // the integrand has degree 2n <= 2p), one block per degree n.
 __global__ void k_n4_delta(int p, const double* __restrict__ tab, const double* __restrict__ rot,
-                           const double* __restrict__ rphi, double* __restrict__ delta) {
+                           const double* __restrict__ rphi, double* __restrict__ delta,
+                           double* __restrict__ deltaT) {
   const TableLayout L(p);
   const int n = blockIdx.x, W = 2 * n + 1, nsn = (p + 1) * L.nphi;
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
@@ -109,6 +110,9 @@ __global__ void k_n4_delta(int p, const double* __restrict__ tab, const double* 
     }
     delta[2 * (n4_doff(n) + e)] = re;
     delta[2 * (n4_doff(n) + e) + 1] = im;
+    const int eT = (m + n) * W + (mp + n);  // transposed copy: rows over m
+    deltaT[2 * (n4_doff(n) + eT)] = re;
+    deltaT[2 * (n4_doff(n) + eT) + 1] = im;
   }
 }
 
@@ -119,6 +123,7 @@ struct N4Args {
   const double* radii;
   const double* coef;    // [ns][nlm][10] exterior coefficients (k_near_coef)
   const double* delta;   // packed Delta_n
+  const double* deltaT;  // packed Delta_n^T (coalesced row products)
   const int* tgt;        // target spheres with >= 1 near neighbour
   const int* nb_off;     // [ns+1]
   const int* nb_idx;     // neighbour sphere indices (ascending)
@@ -127,7 +132,7 @@ struct N4Args {
 
 __host__ __device__ inline int64_t n4_smem_doubles(int p) {
   const int nlm = (p + 1) * (p + 2) / 2, P1 = p + 1;
-  return 8LL * nlm + 8LL * nlm + 8LL * nlm + 6LL * P1 * P1 + 6LL * nlm + 3LL * nlm;
+  return 8LL * nlm + 8LL * nlm + 8LL * nlm + 6LL * P1 * P1 + 6LL * nlm + 3LL * nlm + nlm;
 }
 
 // complex helpers (re, im) in registers
@@ -156,12 +161,24 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
   double* F = CR + 8 * nlm;     // [P1 j][P1 m][3 comp][2]
   double* ACC = F + 6 * P1 * P1;  // [nlm][6]
   double* rt = ACC + 6 * nlm;   // rA, rB, rC
+  // item q (degree-major: q = n(n+1)/2 + m) -> (n, m, lm column); consecutive
+  // threads then share n and walk m, so the rotation matrices are read in
+  // consecutive addresses (Delta^T for the row products, Delta for the column ones)
+  int* nmc = reinterpret_cast<int*>(rt + 3 * nlm);  // [nlm][2]: (n << 16 | m), column
   const int tid = threadIdx.x, nt = blockDim.x;
   const int t = A.tgt[blockIdx.x];
   const double ct_[3] = {A.centres[3 * t], A.centres[3 * t + 1], A.centres[3 * t + 2]};
   const double at = A.radii[t];
   for (int e = tid; e < 3 * nlm; e += nt) rt[e] = A.tab[L.rA + e];
   for (int e = tid; e < 6 * nlm; e += nt) ACC[e] = 0.0;
+  for (int q = tid; q < nlm; q += nt) {
+    int n = 0;
+    while ((n + 1) * (n + 2) / 2 <= q) ++n;
+    const int m = q - n * (n + 1) / 2;
+    nmc[2 * q] = (n << 16) | m;
+    nmc[2 * q + 1] = lm_index(p, n, m);
+  }
+  __syncthreads();
   const double* rA = rt;
   const double* rB = rt + nlm;
   const double* rC = rt + 2 * nlm;
@@ -192,32 +209,30 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
     __syncthreads();
     // ---- (1b) x = Delta (E(alpha) c), rows m' >= 0, then E(beta)
     for (int e = tid; e < 4 * nlm; e += nt) {
-      const int f = e / nlm, c = e - f * nlm;
-      const int2 nm = cofs(c);
-      const int n = nm.x, mp = nm.y;
+      const int f = e / nlm, q = e - f * nlm;
+      const int n = nmc[2 * q] >> 16, mp = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
-      const double* D = A.delta + 2 * n4_doff(n);
+      const double* DT = A.deltaT + 2 * n4_doff(n);
       const int W = 2 * n + 1;
       for (int m = -n; m <= n; ++m) {
         const int am = m < 0 ? -m : m;
         const int cc = f * nlm + lm_index(p, n, am);
         Cx x = {R1[2 * cc], R1[2 * cc + 1]};
         if (m < 0) x.i = -x.i;
-        const int de = (mp + n) * W + (m + n);
-        acc = cfma(Cx{__ldg(D + 2 * de), __ldg(D + 2 * de + 1)}, x, acc);
+        const int de = (m + n) * W + (mp + n);  // Delta[mp][m] from the transpose
+        acc = cfma(Cx{__ldg(DT + 2 * de), __ldg(DT + 2 * de + 1)}, x, acc);
       }
       double sb, cb;
       sincos(mp * beta, &sb, &cb);
       const Cx r = cmul(acc, Cx{cb, sb});
-      R2[2 * e] = r.r;
-      R2[2 * e + 1] = r.i;
+      R2[2 * (f * nlm + c)] = r.r;
+      R2[2 * (f * nlm + c) + 1] = r.i;
     }
     __syncthreads();
     // ---- (1c) c^R = Delta^H (E(beta) Delta E(alpha) c), rows m >= 0 -> CR[c][2 f]
     for (int e = tid; e < 4 * nlm; e += nt) {
-      const int f = e / nlm, c = e - f * nlm;
-      const int2 nm = cofs(c);
-      const int n = nm.x, m = nm.y;
+      const int f = e / nlm, q = e - f * nlm;
+      const int n = nmc[2 * q] >> 16, m = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
       const int W = 2 * n + 1;
@@ -326,32 +341,30 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
     __syncthreads();
     // ---- (3b) x = Delta b^R (rows m' >= 0), then E(-beta)
     for (int e = tid; e < 3 * nlm; e += nt) {
-      const int f = e / nlm, c = e - f * nlm;
-      const int2 nm = cofs(c);
-      const int n = nm.x, mp = nm.y;
+      const int f = e / nlm, q = e - f * nlm;
+      const int n = nmc[2 * q] >> 16, mp = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
-      const double* D = A.delta + 2 * n4_doff(n);
+      const double* DT = A.deltaT + 2 * n4_doff(n);
       const int W = 2 * n + 1;
       for (int m = -n; m <= n; ++m) {
         const int am = m < 0 ? -m : m;
         const int cc = f * nlm + lm_index(p, n, am);
         Cx x = {R1[2 * cc], R1[2 * cc + 1]};
         if (m < 0) x.i = -x.i;
-        const int de = (mp + n) * W + (m + n);
-        acc = cfma(Cx{__ldg(D + 2 * de), __ldg(D + 2 * de + 1)}, x, acc);
+        const int de = (m + n) * W + (mp + n);
+        acc = cfma(Cx{__ldg(DT + 2 * de), __ldg(DT + 2 * de + 1)}, x, acc);
       }
       double sb, cb;
       sincos(mp * beta, &sb, &cb);
       const Cx r = cmul(acc, Cx{cb, -sb});
-      R2[2 * e] = r.r;
-      R2[2 * e + 1] = r.i;
+      R2[2 * (f * nlm + c)] = r.r;
+      R2[2 * (f * nlm + c) + 1] = r.i;
     }
     __syncthreads();
     // ---- (3c) b = E(-alpha) Delta^H (...), rows m >= 0; accumulate
     for (int e = tid; e < 3 * nlm; e += nt) {
-      const int f = e / nlm, c = e - f * nlm;
-      const int2 nm = cofs(c);
-      const int n = nm.x, m = nm.y;
+      const int f = e / nlm, q = e - f * nlm;
+      const int n = nmc[2 * q] >> 16, m = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
       const int W = 2 * n + 1;

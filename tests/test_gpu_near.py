@@ -18,9 +18,10 @@ def bie():
     return m
 
 
-def gpu_apply_near(bie, c, a, p, mu, f, q, eta, parts=3):
+def gpu_apply_near(bie, c, a, p, mu, f, q, eta, parts=3, excl=-1):
     ctx = bie.bie_create(c, a, p, mu)
     bie.bie_set_near(ctx, eta)
+    bie.bie_set_near_exclusion(ctx, excl)
     npairs = bie.bie_near_pairs(ctx)
     u = torch.full((len(a) * (p + 1) * (2 * p + 2), 3), np.nan, dtype=torch.float64, device="cuda")
     bie.bie_apply_parts(ctx, _dev(f), _dev(q), u, parts)
@@ -47,10 +48,13 @@ def test_near_two_spheres_close(bie, oracle_mod):
     _assert_parity(got, oracle_mod.apply_near(c, a, p, mu, f, q, 1.0), "near 2 spheres")
 
 
+@pytest.mark.parametrize("excl", [0, 1])
 @pytest.mark.parametrize("p,ns,eta", [(4, 6, 0.5), (6, 8, 1.0), (5, 5, 2.0), (12, 3, 1.0)])
-def test_near_random_suspensions(bie, oracle_mod, p, ns, eta):
+def test_near_random_suspensions(bie, oracle_mod, p, ns, eta, excl):
+    """Both treatments of the near pairs' smooth rule (bie_set_near_exclusion:
+    0 subtracted by k_near, 1 skipped inside the far-field kernel)."""
     c, a, f, q, mu = _random_case(300 + p + ns, ns, p, True, 0.9)
-    got, npairs = gpu_apply_near(bie, c, a, p, mu, f, q, eta)
+    got, npairs = gpu_apply_near(bie, c, a, p, mu, f, q, eta, excl=excl)
     assert npairs == _count_pairs(oracle_mod, c, a, eta)
     _assert_parity(got, oracle_mod.apply_near(c, a, p, mu, f, q, eta), f"near p={p} eta={eta}")
 

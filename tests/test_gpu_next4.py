@@ -22,10 +22,11 @@ def bie():
     return m
 
 
-def gpu_apply_mode(bie, c, a, p, mu, f, q, eta, mode, parts=3, variant=0):
+def gpu_apply_mode(bie, c, a, p, mu, f, q, eta, mode, parts=3, variant=0, excl=-1):
     ctx = bie.bie_create(c, a, p, mu)
     bie.bie_set_self_kernel(ctx, variant)
     bie.bie_set_near(ctx, eta)
+    bie.bie_set_near_exclusion(ctx, excl)
     bie.bie_set_near_mode(ctx, mode)
     N = len(a) * (p + 1) * (2 * p + 2)
     u = torch.full((N, 3), np.nan, dtype=torch.float64, device="cuda")
@@ -47,13 +48,14 @@ def test_next4_two_spheres_oblique(bie, oracle_mod):
     _assert_parity(got, oracle_mod.apply_near4(c, a, p, mu, f, q, 1.0), "next4 2 spheres")
 
 
-@pytest.mark.parametrize("p,ns,eta,variant", [(4, 5, 1.0, 0), (6, 6, 1.0, 0), (5, 5, 2.0, 1), (8, 4, 1.0, 2),
-                                              (9, 3, 1.5, 0), (12, 3, 1.0, 0)])
-def test_next4_random_suspensions(bie, oracle_mod, p, ns, eta, variant):
+@pytest.mark.parametrize("p,ns,eta,variant,excl", [(4, 5, 1.0, 0, 1), (6, 6, 1.0, 0, 0), (5, 5, 2.0, 1, 1),
+                                                   (8, 4, 1.0, 2, 0), (9, 3, 1.5, 0, 1), (12, 3, 1.0, 0, 0)])
+def test_next4_random_suspensions(bie, oracle_mod, p, ns, eta, variant, excl):
     """Polydisperse random suspensions; self-kernel variants 0/1 (k_sht) and 2
-    (round-1 kernel: the NEXT-4 coefficient pass then runs on k_sht)."""
+    (round-1 kernel: the NEXT-4 coefficient pass then runs on k_sht); the near
+    pairs' smooth rule subtracted (excl 0) or skipped in the far field (1)."""
     c, a, f, q, mu = _random_case(500 + p + ns, ns, p, True, 0.9)
-    got = gpu_apply_mode(bie, c, a, p, mu, f, q, eta, 1, variant=variant)
+    got = gpu_apply_mode(bie, c, a, p, mu, f, q, eta, 1, variant=variant, excl=excl)
     _assert_parity(got, oracle_mod.apply_near4(c, a, p, mu, f, q, eta), f"next4 p={p} eta={eta}")
 
 

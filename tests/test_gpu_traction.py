@@ -102,9 +102,10 @@ def test_completion_part_only_for_K(bie):
 
 
 # ---------------------------------------------- near-singular correction of K
-def gpu_K_near(bie, c, a, p, mu, sigma, eta, parts=3):
+def gpu_K_near(bie, c, a, p, mu, sigma, eta, parts=3, excl=-1):
     ctx = bie.bie_create(c, a, p, mu)
     bie.bie_set_near(ctx, eta)
+    bie.bie_set_near_exclusion(ctx, excl)
     u = torch.full((len(sigma), 3), np.nan, dtype=torch.float64, device="cuda")
     bie.bie_apply_K(ctx, _dev(sigma), u, parts)
     torch.cuda.synchronize()
@@ -112,11 +113,13 @@ def gpu_K_near(bie, c, a, p, mu, sigma, eta, parts=3):
     return u.cpu().numpy()
 
 
+@pytest.mark.parametrize("excl", [0, 1])
 @pytest.mark.parametrize("p,ns,eta", [(4, 6, 1.0), (6, 8, 2.0), (8, 5, 0.7), (12, 4, 1.0), (3, 10, 3.0)])
-def test_K_near_matches_oracle(bie, oracle_mod, p, ns, eta):
+def test_K_near_matches_oracle(bie, oracle_mod, p, ns, eta, excl):
+    """Near pairs' smooth K sum subtracted (excl 0) or skipped in the far field (1)."""
     c, a, f, _, mu = _random_case(1100 + p, ns, p, True, 0.9)
     ref = oracle_mod.apply_K_near(c, a, p, f, eta)
-    _assert_parity(gpu_K_near(bie, c, a, p, mu, f, eta), ref, f"K near p={p} eta={eta}")
+    _assert_parity(gpu_K_near(bie, c, a, p, mu, f, eta, excl=excl), ref, f"K near p={p} eta={eta}")
     if p == 6:  # with the completion operator as well
         _assert_parity(gpu_K_near(bie, c, a, p, mu, f, eta, parts=7),
                        ref + oracle_mod.completion(c, a, p, f), "K near + L")
