@@ -239,6 +239,18 @@ int bie_reset_profile(bie_ctx* ctx);
  */
 int bie_set_near(bie_ctx* ctx, double eta);
 
+/*
+ * Host utility (no GPU needed): the CSR neighbour lists bie_set_near builds --
+ * for every target sphere t the source spheres s != t failing eq 4.5 (P:323-
+ * 328) in the IEEE evaluation order |c_s - c_t| - a_s - a_t < eta max(2 a_s,
+ * 2 a_t), ascending -- from a uniform cell list (cell = 2 a_max (1 + eta)).
+ * off_h [n_spheres + 1] (int64) is always filled and *total set; idx_h (cap
+ * entries, may be NULL) receives the lists.  BIE_ERR_ARG on bad arguments or
+ * cap < *total (off_h and *total are still valid then).
+ */
+int bie_near_lists(const double* centres_h, const double* radii_h, int64_t n_spheres, double eta,
+                   int64_t* off_h, int* idx_h, int64_t cap, int64_t* total);
+
 /* Number of (target sphere, source sphere) near pairs of the current eta; -1 for NULL. */
 int64_t bie_near_pairs(const bie_ctx* ctx);
 

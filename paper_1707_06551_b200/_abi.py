@@ -24,6 +24,7 @@ SYMBOLS = (
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
     "bie_set_self_kernel", "bie_set_near_mode", "bie_set_near_exclusion", "bie_set_far_reduction",
+    "bie_near_lists",
     "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K", "bie_eval_traction",
     "bie_status_string", "bie_last_error",
 )
@@ -58,6 +59,7 @@ _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
 _lib.bie_set_self_kernel.argtypes = [_vp, _i32]
 _lib.bie_set_near_mode.argtypes = [_vp, _i32]
 _lib.bie_set_near_exclusion.argtypes = [_vp, _i32]
+_lib.bie_near_lists.argtypes = [_vp, _vp, _i64, _d, _vp, _vp, _i64, ctypes.POINTER(_i64)]
 _lib.bie_set_far_reduction.argtypes = [_vp, _i32]
 _lib.bie_set_near.argtypes = [_vp, _d]
 _lib.bie_near_pairs.argtypes = [_vp]
@@ -286,6 +288,26 @@ def bie_set_self_kernel(ctx, variant: int):
 def bie_set_far_reduction(ctx, mode: int):
     """Far-field schedule: 1 chunk partials + k_reduce (default), 0 stream-K, 2/3/4 clusters of 8/4/16."""
     _check(ctx, _lib.bie_set_far_reduction(ctx.handle, int(mode)))
+
+
+def bie_near_lists(centres, radii, eta: float):
+    """Host-side CSR neighbour lists of eq 4.5 (no GPU): (off [n+1], idx)."""
+    import numpy as np
+    c = np.ascontiguousarray(centres, dtype=np.float64).reshape(-1, 3)
+    a = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+    n = len(a)
+    off = np.zeros(n + 1, dtype=np.int64)
+    total = _i64(0)
+    rc = _lib.bie_near_lists(c.ctypes.data, a.ctypes.data, n, float(eta), off.ctypes.data, None, 0,
+                             ctypes.byref(total))
+    if rc:
+        raise BieError(rc, "bie_near_lists")
+    idx = np.zeros(max(total.value, 1), dtype=np.int32)
+    rc = _lib.bie_near_lists(c.ctypes.data, a.ctypes.data, n, float(eta), off.ctypes.data, idx.ctypes.data,
+                             len(idx), ctypes.byref(total))
+    if rc:
+        raise BieError(rc, "bie_near_lists")
+    return off, idx[: total.value]
 
 
 def bie_set_near_exclusion(ctx, mode: int):

@@ -1464,6 +1464,22 @@ int bie_set_near(bie_ctx* c, double eta) {
 
 int64_t bie_near_pairs(const bie_ctx* c) { return c ? c->n_near_pairs : -1; }
 
+int bie_near_lists(const double* centres_h, const double* radii_h, int64_t n_spheres, double eta,
+                   int64_t* off_h, int* idx_h, int64_t cap, int64_t* total) {
+  if (!centres_h || !radii_h || n_spheres < 1 || !off_h || !total || !(eta >= 0.0) || !std::isfinite(eta))
+    return BIE_ERR_ARG;
+  std::vector<int64_t> off;
+  std::vector<int> idx;
+  near_lists_host(centres_h, radii_h, n_spheres, eta, off, idx);
+  *total = off[n_spheres];
+  for (int64_t t = 0; t <= n_spheres; ++t) off_h[t] = off[t];
+  if (idx_h) {
+    if (cap < off[n_spheres]) return BIE_ERR_ARG;
+    for (size_t k = 0; k < idx.size(); ++k) idx_h[k] = idx[k];
+  }
+  return BIE_OK;
+}
+
 int bie_set_near_exclusion(bie_ctx* c, int mode) {
   if (!c) return BIE_ERR_ARG;
   if (mode < -1 || mode > 1) return fail(c, BIE_ERR_ARG, "near exclusion must be -1, 0 or 1%s");

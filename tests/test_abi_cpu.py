@@ -93,3 +93,23 @@ def test_package_has_no_cpu_fallback():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "import oracle" not in src and "from oracle" not in src, fn
+
+
+@pytest.mark.parametrize("seed,ns,eta,poly", [(1, 60, 1.0, True), (2, 120, 0.5, False), (3, 40, 3.0, True),
+                                              (4, 1, 1.0, False), (5, 120, 0.0, True)])
+def test_near_lists_match_bruteforce_eq45(abi, oracle_mod, seed, ns, eta, poly):
+    """The host cell-list neighbour builder (bie_near_lists; what bie_set_near
+    uploads) equals the brute-force eq 4.5 test of the oracle (oracle.is_near)
+    over all ordered pairs, ascending per target; eta = 0 gives no pairs."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.5, 1.5, ns) if poly else np.ones(ns)
+    c = []
+    while len(c) < ns:
+        x = rng.uniform(0, 3.2 * ns ** (1 / 3) + 2, 3)
+        if all(np.linalg.norm(x - y) > a[len(c)] + a[j] + 0.05 for j, y in enumerate(c)):
+            c.append(x)
+    c = np.array(c)
+    off, idx = abi.bie_near_lists(c, a, eta)
+    for t in range(ns):
+        ref = [s for s in range(ns) if s != t and oracle_mod.is_near(c[s], a[s], c[t], a[t], eta)]
+        assert list(idx[off[t]:off[t + 1]]) == ref, t
