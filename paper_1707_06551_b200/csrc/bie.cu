@@ -358,8 +358,12 @@ static void self_launch(bie_ctx* c, const SelfArgs& SA, cudaStream_t s) {
     launch_self(SA, s);
     return;
   }
+  if (variant == 3 && !SA.psinear) {
+    launch_self2(SA, s);
+    return;
+  }
   // (NEXT-4's coefficient accumulation exists only in k_sht)
-  const cudaError_t e = launch_sht(SA, c->d_sht, variant == 2 ? 0 : variant, c->sm_count, c->sht_occ, s);
+  const cudaError_t e = launch_sht(SA, c->d_sht, variant >= 2 ? 0 : variant, c->sm_count, c->sht_occ, s);
   (void)e;  // surfaced by the caller's launch_check (cudaGetLastError)
 }
 
@@ -1752,7 +1756,9 @@ int bie_set_far_reduction(bie_ctx* c, int mode) {
 
 int bie_set_self_kernel(bie_ctx* c, int variant) {
   if (!c) return BIE_ERR_ARG;
-  if (variant < -1 || variant > 2) return fail(c, BIE_ERR_ARG, "self kernel variant must be -1, 0, 1 or 2%s");
+  if (variant < -1 || variant > 3) return fail(c, BIE_ERR_ARG, "self kernel variant must be -1..3%s");
+  if (variant == 3 && self2_smem_bytes(c->p) > 227 * 1024)
+    return fail(c, BIE_ERR_UNSUPPORTED, "two spheres per CTA exceed shared memory at this order%s");
   c->self_variant = variant;
   return BIE_OK;
 }

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
     __syncthreads();
     // ---- (1b) x = Delta (E(alpha) c), rows m' >= 0, then E(beta)
     for (int e = tid; e < 4 * nlm; e += nt) {
-      const int f = e / nlm, q = e - f * nlm;
+      const int f = e & 3, q = e >> 2;  // families fastest: 4 lanes share each matrix entry
       const int n = nmc[2 * q] >> 16, mp = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
       const double* DT = A.deltaT + 2 * n4_doff(n);
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
     __syncthreads();
     // ---- (1c) c^R = Delta^H (E(beta) Delta E(alpha) c), rows m >= 0 -> CR[c][2 f]
     for (int e = tid; e < 4 * nlm; e += nt) {
-      const int f = e / nlm, q = e - f * nlm;
+      const int f = e & 3, q = e >> 2;  // families fastest: 4 lanes share each matrix entry
       const int n = nmc[2 * q] >> 16, m = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
     __syncthreads();
     // ---- (3b) x = Delta b^R (rows m' >= 0), then E(-beta)
     for (int e = tid; e < 3 * nlm; e += nt) {
-      const int f = e / nlm, q = e - f * nlm;
+      const int q = e / 3, f = e - 3 * q;  // families fastest: 3 lanes share each matrix entry
       const int n = nmc[2 * q] >> 16, mp = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
       const double* DT = A.deltaT + 2 * n4_doff(n);
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(128) k_n4(const N4Args A) {
     __syncthreads();
     // ---- (3c) b = E(-alpha) Delta^H (...), rows m >= 0; accumulate
     for (int e = tid; e < 3 * nlm; e += nt) {
-      const int f = e / nlm, q = e - f * nlm;
+      const int q = e / 3, f = e - 3 * q;  // families fastest: 3 lanes share each matrix entry
       const int n = nmc[2 * q] >> 16, m = nmc[2 * q] & 0xFFFF, c = nmc[2 * q + 1];
       Cx acc = {0.0, 0.0};
       const double* D = A.delta + 2 * n4_doff(n);

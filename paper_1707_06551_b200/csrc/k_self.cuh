@@ -56,22 +56,35 @@ __host__ __device__ inline int64_t self_smem_doubles(int p) {
 
 // PT > 0: the order p is the compile-time constant PT (loop bounds, index
 // decoding and strides fold away); PT = 0: generic runtime p.
-template <int TPB, int MINB, int PT = 0>
+// SPC: spheres per CTA.  Each phase's item loop handles the same item of all
+// SPC spheres back to back -- independent work the scheduler interleaves
+// (latency hiding within a thread) -- sharing the phase barriers.
+template <int TPB, int MINB, int PT = 0, int SPC = 1>
 __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   extern __shared__ __align__(16) double sm[];
   const int p = PT > 0 ? PT : A.p, P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
   const TableLayout L(p);
   const int nlm = L.nlm;
-  double* C = sm;                          // [2][3][nsn]
-  double* F = C + 6 * nsn;                 // [2][3][P1][P1][2]
-  double* PSI = F;                         // [nlm][3][2]; aliases F (dead after phase C)
-  double2* tw = reinterpret_cast<double2*>(F + 12 * P1 * P1);  // (cos, sin)(2 pi q/nphi)
-  double* U = C;                           // [3][P1][P1][2] (C is dead after B)
+  const int SZ = 6 * nsn + 12 * P1 * P1;  // per sphere: C [2][3][nsn] + F [2][3][P1][P1][2]
+  double2* tw = reinterpret_cast<double2*>(sm + SPC * SZ);  // (cos, sin)(2 pi q/nphi), shared
+  // per-sphere views: C; F (PSI aliases F, dead after phase C); U aliases C
+  auto Cp = [&](int sp) { return sm + sp * SZ; };
+  auto Fp_ = [&](int sp) { return sm + sp * SZ + 6 * nsn; };
   const double* __restrict__ tab = A.tab;
-  const int64_t s = blockIdx.x;
-  const double a = A.radii[s];
-  const double cx = A.centres[3 * s], cy = A.centres[3 * s + 1], cz = A.centres[3 * s + 2];
-  const double aS = a / A.mu;
+  int64_t sidx[SPC];
+  bool valid[SPC];
+  double ra[SPC], rcx[SPC], rcy[SPC], rcz[SPC], raS[SPC];
+#pragma unroll
+  for (int sp = 0; sp < SPC; ++sp) {
+    sidx[sp] = (int64_t)blockIdx.x * SPC + sp;
+    valid[sp] = sidx[sp] < A.ns;
+    const int64_t sc = valid[sp] ? sidx[sp] : A.ns - 1;
+    ra[sp] = A.radii[sc];
+    rcx[sp] = A.centres[3 * sc];
+    rcy[sp] = A.centres[3 * sc + 1];
+    rcz[sp] = A.centres[3 * sc + 2];
+    raS[sp] = ra[sp] / A.mu;
+  }
   const double cS = 1.0 / (8.0 * kPi * A.mu), cD = 3.0 / (4.0 * kPi);
   const int tid = threadIdx.x, nt = blockDim.x;
 
@@ -82,56 +95,67 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   //   C[k] = g(k) + g(nphi-k),  C[nphi-k] = g(k) - g(nphi-k)   (k = 1..p),
   //   C[0] = g(0),  C[P1] = g(P1)  -- halving the DFT's multiply-adds.
   const bool spec = A.self || A.alpha;
-  auto node = [&](int j, int k, double* g) {
+  auto node = [&](int sp, int j, int k, double* g) {
     const int kk = j * nphi + k;
+    const int64_t s = sidx[sp];
     const int64_t i = s * nsn + kk;
+    const double a = ra[sp], aS = raS[sp];
     double f0 = 0, f1 = 0, f2 = 0, q0 = 0, q1 = 0, q2 = 0;
     if (A.f) { f0 = A.f[3 * i]; f1 = A.f[3 * i + 1]; f2 = A.f[3 * i + 2]; }
     if (A.q) { q0 = A.q[3 * i]; q1 = A.q[3 * i + 1]; q2 = A.q[3 * i + 2]; }
     const double ct = tab[L.t + j], st = tab[L.st + j];
-    const double cp = tw[k].x, sp = tw[k].y;
-    const double n0 = st * cp, n1 = st * sp, n2 = ct;
+    const double cp = tw[k].x, sp_ = tw[k].y;
+    const double n0 = st * cp, n1 = st * sp_, n2 = ct;
     const double w = a * a * tab[L.wu + j];
     // packed source record (row a2)
     double2* r2 = reinterpret_cast<double2*>(A.rec + i * kRec);
     const double ws = w * cS, wd = w * cD;
-    r2[0] = make_double2(cx + a * n0, cy + a * n1);
-    r2[1] = make_double2(cz + a * n2, n0);
+    r2[0] = make_double2(rcx[sp] + a * n0, rcy[sp] + a * n1);
+    r2[1] = make_double2(rcz[sp] + a * n2, n0);
     r2[2] = make_double2(n1, n2);
     r2[3] = make_double2(ws * f0, ws * f1);
     r2[4] = make_double2(ws * f2, wd * q0);
     r2[5] = make_double2(wd * q1, wd * q2);
     // e_r = n, e_theta = (ct cp, ct sp, -st), e_phi = (-sp, cp, 0)
     g[0] = aS * (f0 * n0 + f1 * n1 + f2 * n2);
-    g[1] = aS * (f0 * ct * cp + f1 * ct * sp - f2 * st);
-    g[2] = aS * (-f0 * sp + f1 * cp);
+    g[1] = aS * (f0 * ct * cp + f1 * ct * sp_ - f2 * st);
+    g[2] = aS * (-f0 * sp_ + f1 * cp);
     g[3] = q0 * n0 + q1 * n1 + q2 * n2;
-    g[4] = q0 * ct * cp + q1 * ct * sp - q2 * st;
-    g[5] = -q0 * sp + q1 * cp;
+    g[4] = q0 * ct * cp + q1 * ct * sp_ - q2 * st;
+    g[5] = -q0 * sp_ + q1 * cp;
   };
   __syncthreads();  // tw ready
   for (int it = tid; it < P1 * (P1 + 1); it += nt) {
     const int j = it / (P1 + 1), k = it - j * (P1 + 1);
     const bool pair = k > 0 && k < P1;
-    double g1[6], g2[6];
-    node(j, k, g1);
-    if (pair) node(j, nphi - k, g2);
-    if (spec) {
-      double* row = C + j * nphi;
 #pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        if (pair) {
-          row[d * nsn + k] = g1[d] + g2[d];
-          row[d * nsn + nphi - k] = g1[d] - g2[d];
-        } else {
-          row[d * nsn + k] = g1[d];
+    for (int sp = 0; sp < SPC; ++sp) {
+      if (!valid[sp]) continue;
+      double g1[6], g2[6];
+      node(sp, j, k, g1);
+      if (pair) node(sp, j, nphi - k, g2);
+      if (spec) {
+        double* row = Cp(sp) + j * nphi;
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+          if (pair) {
+            row[d * nsn + k] = g1[d] + g2[d];
+            row[d * nsn + nphi - k] = g1[d] - g2[d];
+          } else {
+            row[d * nsn + k] = g1[d];
+          }
         }
       }
     }
   }
+  auto zero_u = [&]() {
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp)
+      if (valid[sp] && A.u)
+        for (int e = tid; e < 3 * nsn; e += nt) A.u[sidx[sp] * 3 * nsn + e] = 0.0;
+  };
   if (!spec) {
-    if (A.u)
-      for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
+    zero_u();
     return;
   }
   __syncthreads();
@@ -146,27 +170,31 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
       const int mh = it % H, row = it / H;
       const int m1 = mh, m2 = mh + H;
       const bool two = m2 < P1;
-      const double* g = C + row * nphi;
-      double re1 = (m1 & 1) ? g[0] - g[P1] : g[0] + g[P1], im1 = 0.0;
-      double re2 = (m2 & 1) ? g[0] - g[P1] : g[0] + g[P1], im2 = 0.0;
-      int i1 = m1, i2 = two ? m2 : 0;
-      for (int k = 1; k <= p; ++k) {
-        const double gs = g[k], gd = g[nphi - k];
-        const double2 t1 = tw[i1], t2 = tw[i2];
-        re1 = fma(gs, t1.x, re1);
-        im1 = fma(-gd, t1.y, im1);
-        re2 = fma(gs, t2.x, re2);
-        im2 = fma(-gd, t2.y, im2);
-        i1 += m1;
-        if (i1 >= nphi) i1 -= nphi;
-        i2 += m2;
-        if (i2 >= nphi) i2 -= nphi;
-      }
-      F[2 * (row * P1 + m1)] = re1;
-      F[2 * (row * P1 + m1) + 1] = im1;
-      if (two) {
-        F[2 * (row * P1 + m2)] = re2;
-        F[2 * (row * P1 + m2) + 1] = im2;
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp) {
+        const double* g = Cp(sp) + row * nphi;
+        double* F = Fp_(sp);
+        double re1 = (m1 & 1) ? g[0] - g[P1] : g[0] + g[P1], im1 = 0.0;
+        double re2 = (m2 & 1) ? g[0] - g[P1] : g[0] + g[P1], im2 = 0.0;
+        int i1 = m1, i2 = two ? m2 : 0;
+        for (int k = 1; k <= p; ++k) {
+          const double gs = g[k], gd = g[nphi - k];
+          const double2 t1 = tw[i1], t2 = tw[i2];
+          re1 = fma(gs, t1.x, re1);
+          im1 = fma(-gd, t1.y, im1);
+          re2 = fma(gs, t2.x, re2);
+          im2 = fma(-gd, t2.y, im2);
+          i1 += m1;
+          if (i1 >= nphi) i1 -= nphi;
+          i2 += m2;
+          if (i2 >= nphi) i2 -= nphi;
+        }
+        F[2 * (row * P1 + m1)] = re1;
+        F[2 * (row * P1 + m1) + 1] = im1;
+        if (two) {
+          F[2 * (row * P1 + m2)] = re2;
+          F[2 * (row * P1 + m2) + 1] = im2;
+        }
       }
     }
   }
@@ -174,39 +202,46 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // ---------------------------------------------------------------- C
   // Projection per (density, n, m): ALPHA[d][c] = (<F,Y e_r>, <F,G>, <F,X>),
   // complex.  ALPHA aliases C, which is dead after phase B.
-  double* ALPHA = C;  // [2][nlm][3][2]
   for (int it = tid; it < 2 * nlm; it += nt) {
     const int d = it / nlm, c = it - d * nlm;
     int m = 0, off = 0;
     while (off + (P1 - m) <= c) { off += P1 - m; ++m; }
-    double y0 = 0, y1 = 0, g0 = 0, g1 = 0, x0 = 0, x1 = 0;
+    double y0[SPC], y1[SPC], g0[SPC], g1[SPC], x0[SPC], x1[SPC];
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp) y0[sp] = y1[sp] = g0[sp] = g1[sp] = x0[sp] = x1[sp] = 0.0;
     for (int j = 0; j < P1; ++j) {
       const double wj = tab[L.wu + j];
       const double Pv = wj * tab[L.P + (int64_t)j * nlm + c];
       const double dPv = wj * tab[L.dP + (int64_t)j * nlm + c];
       const double mPv = wj * tab[L.mPs + (int64_t)j * nlm + c];
-      const double* Fr = F + 2 * (((3 * d + 0) * P1 + j) * P1 + m);
-      const double* Ft = F + 2 * (((3 * d + 1) * P1 + j) * P1 + m);
-      const double* Fp = F + 2 * (((3 * d + 2) * P1 + j) * P1 + m);
-      y0 = fma(Pv, Fr[0], y0);                        // <F, Y e_r>
-      y1 = fma(Pv, Fr[1], y1);
-      g0 = fma(dPv, Ft[0], fma(mPv, Fp[1], g0));      // <F, G> = dP F_t - i mP F_p
-      g1 = fma(dPv, Ft[1], fma(-mPv, Fp[0], g1));
-      x0 = fma(dPv, Fp[0], fma(-mPv, Ft[1], x0));     // <F, X> = dP F_p + i mP F_t
-      x1 = fma(dPv, Fp[1], fma(mPv, Ft[0], x1));
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp) {
+        const double* F = Fp_(sp);
+        const double* Fr = F + 2 * (((3 * d + 0) * P1 + j) * P1 + m);
+        const double* Ft = F + 2 * (((3 * d + 1) * P1 + j) * P1 + m);
+        const double* Fp = F + 2 * (((3 * d + 2) * P1 + j) * P1 + m);
+        y0[sp] = fma(Pv, Fr[0], y0[sp]);                          // <F, Y e_r>
+        y1[sp] = fma(Pv, Fr[1], y1[sp]);
+        g0[sp] = fma(dPv, Ft[0], fma(mPv, Fp[1], g0[sp]));        // <F, G> = dP F_t - i mP F_p
+        g1[sp] = fma(dPv, Ft[1], fma(-mPv, Fp[0], g1[sp]));
+        x0[sp] = fma(dPv, Fp[0], fma(-mPv, Ft[1], x0[sp]));       // <F, X> = dP F_p + i mP F_t
+        x1[sp] = fma(dPv, Fp[1], fma(mPv, Ft[0], x1[sp]));
+      }
     }
-    double* o = ALPHA + 6 * it;
-    o[0] = y0; o[1] = y1; o[2] = g0; o[3] = g1; o[4] = x0; o[5] = x1;
-    if (A.alpha) {
-      double2* g2 = reinterpret_cast<double2*>(A.alpha + (s * 2 * nlm + it) * 6);
-      g2[0] = make_double2(y0, y1);
-      g2[1] = make_double2(g0, g1);
-      g2[2] = make_double2(x0, x1);
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp) {
+      double* o = Cp(sp) + 6 * it;  // ALPHA [2][nlm][3][2]
+      o[0] = y0[sp]; o[1] = y1[sp]; o[2] = g0[sp]; o[3] = g1[sp]; o[4] = x0[sp]; o[5] = x1[sp];
+      if (A.alpha && valid[sp]) {
+        double2* g2 = reinterpret_cast<double2*>(A.alpha + (sidx[sp] * 2 * nlm + it) * 6);
+        g2[0] = make_double2(y0[sp], y1[sp]);
+        g2[1] = make_double2(g0[sp], g1[sp]);
+        g2[2] = make_double2(x0[sp], x1[sp]);
+      }
     }
   }
   if (!A.self) {
-    if (A.u)
-      for (int e = tid; e < 3 * nsn; e += nt) A.u[s * 3 * nsn + e] = 0.0;
+    zero_u();
     return;
   }
   __syncthreads();
@@ -221,33 +256,38 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     const double* lD = tab + L.lamD + 3 * n;
     const double inn = n ? 1.0 / ((double)n * (n + 1)) : 0.0;
     const double i2n = 1.0 / (2.0 * n + 1.0);
-    const double* af = ALPHA + 6 * c;
-    const double* aq = ALPHA + 6 * (nlm + c);
-    double* o = PSI + 6 * c;
 #pragma unroll
-    for (int ri = 0; ri < 2; ++ri) {
-      double aV[2], aW[2], aX[2];
-      const double* al[2] = {af, aq};
+    for (int sp = 0; sp < SPC; ++sp) {
+      const double* ALPHA = Cp(sp);
+      const double* af = ALPHA + 6 * c;
+      const double* aq = ALPHA + 6 * (nlm + c);
+      double* o = Fp_(sp) + 6 * c;  // PSI
+      const double aS = raS[sp];
 #pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        const double phY = al[d][ri], phG = al[d][2 + ri] * inn, phX = al[d][4 + ri] * inn;
-        aV[d] = (n * phG - phY) * i2n;          // eq 2.13
-        aW[d] = ((n + 1) * phG + phY) * i2n;    // eq 2.14
-        aX[d] = phX;
+      for (int ri = 0; ri < 2; ++ri) {
+        double aV[2], aW[2], aX[2];
+        const double* al[2] = {af, aq};
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const double phY = al[d][ri], phG = al[d][2 + ri] * inn, phX = al[d][4 + ri] * inn;
+          aV[d] = (n * phG - phY) * i2n;          // eq 2.13
+          aW[d] = ((n + 1) * phG + phY) * i2n;    // eq 2.14
+          aX[d] = phX;
+        }
+        double psV, psW, psX;
+        if (A.precond) {  // (1/sigma - 2) on the degree-<=p modes; +2 x added in phase E
+          psV = (1.0 / (0.5 + lS[0] * aS + lD[0]) - 2.0) * aV[1];
+          psW = n ? (1.0 / (0.5 + lS[1] * aS + lD[1]) - 2.0) * aW[1] : 0.0;
+          psX = n ? (1.0 / (0.5 + lS[2] * aS + lD[2]) - 2.0) * aX[1] : 0.0;
+        } else {
+          psV = lS[0] * aV[0] + lD[0] * aV[1];
+          psW = lS[1] * aW[0] + lD[1] * aW[1];
+          psX = lS[2] * aX[0] + lD[2] * aX[1];
+        }
+        o[0 + ri] = -(n + 1.0) * psV + n * psW;  // psi^Y (eq 2.17)
+        o[2 + ri] = psV + psW;                   // psi^G (eq 2.16)
+        o[4 + ri] = psX;                         // psi^X
       }
-      double psV, psW, psX;
-      if (A.precond) {  // (1/sigma - 2) on the degree-<=p modes; +2 x added in phase E
-        psV = (1.0 / (0.5 + lS[0] * aS + lD[0]) - 2.0) * aV[1];
-        psW = n ? (1.0 / (0.5 + lS[1] * aS + lD[1]) - 2.0) * aW[1] : 0.0;
-        psX = n ? (1.0 / (0.5 + lS[2] * aS + lD[2]) - 2.0) * aX[1] : 0.0;
-      } else {
-        psV = lS[0] * aV[0] + lD[0] * aV[1];
-        psW = lS[1] * aW[0] + lD[1] * aW[1];
-        psX = lS[2] * aX[0] + lD[2] * aX[1];
-      }
-      o[0 + ri] = -(n + 1.0) * psV + n * psW;  // psi^Y (eq 2.17)
-      o[2 + ri] = psV + psW;                   // psi^G (eq 2.16)
-      o[4 + ri] = psX;                         // psi^X
     }
   }
   __syncthreads();
@@ -264,29 +304,47 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     const double* mPj = tab + L.mPs + (int64_t)j * nlm;
     const int o = j * P1 + m;
     if (half == 0) {
-      double a0 = 0, a1 = 0;
+      double a0[SPC], a1[SPC];
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp) a0[sp] = a1[sp] = 0.0;
       for (int c = c0; c < c0 + (P1 - m); ++c) {
         const double pv = __ldg(Pj + c);
-        const double* ps = PSI + 6 * c;
-        a0 = fma(ps[0], pv, a0);
-        a1 = fma(ps[1], pv, a1);
+#pragma unroll
+        for (int sp = 0; sp < SPC; ++sp) {
+          const double* ps = Fp_(sp) + 6 * c;
+          a0[sp] = fma(ps[0], pv, a0[sp]);
+          a1[sp] = fma(ps[1], pv, a1[sp]);
+        }
       }
-      U[2 * o] = a0;
-      U[2 * o + 1] = a1;
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp) {
+        double* U = Cp(sp);
+        U[2 * o] = a0[sp];
+        U[2 * o + 1] = a1[sp];
+      }
     } else {
-      double t0 = 0, t1 = 0, q0 = 0, q1 = 0;
+      double t0[SPC], t1[SPC], q0[SPC], q1[SPC];
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp) t0[sp] = t1[sp] = q0[sp] = q1[sp] = 0.0;
       for (int c = c0; c < c0 + (P1 - m); ++c) {
         const double dp = __ldg(dPj + c), mp = __ldg(mPj + c);
-        const double* ps = PSI + 6 * c;
-        t0 = fma(ps[2], dp, fma(ps[5], mp, t0));
-        t1 = fma(ps[3], dp, fma(-ps[4], mp, t1));
-        q0 = fma(ps[4], dp, fma(-ps[3], mp, q0));
-        q1 = fma(ps[5], dp, fma(ps[2], mp, q1));
+#pragma unroll
+        for (int sp = 0; sp < SPC; ++sp) {
+          const double* ps = Fp_(sp) + 6 * c;
+          t0[sp] = fma(ps[2], dp, fma(ps[5], mp, t0[sp]));
+          t1[sp] = fma(ps[3], dp, fma(-ps[4], mp, t1[sp]));
+          q0[sp] = fma(ps[4], dp, fma(-ps[3], mp, q0[sp]));
+          q1[sp] = fma(ps[5], dp, fma(ps[2], mp, q1[sp]));
+        }
       }
-      U[2 * (P1 * P1 + o)] = t0;
-      U[2 * (P1 * P1 + o) + 1] = t1;
-      U[2 * (2 * P1 * P1 + o)] = q0;
-      U[2 * (2 * P1 * P1 + o) + 1] = q1;
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp) {
+        double* U = Cp(sp);
+        U[2 * (P1 * P1 + o)] = t0[sp];
+        U[2 * (P1 * P1 + o) + 1] = t1[sp];
+        U[2 * (2 * P1 * P1 + o)] = q0[sp];
+        U[2 * (2 * P1 * P1 + o) + 1] = q1[sp];
+      }
     }
   }
   __syncthreads();
@@ -297,44 +355,57 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // then spherical -> Cartesian components and the store of u_self.
   for (int it = tid; it < P1 * (P1 + 1); it += nt) {
     const int j = it / (P1 + 1), k = it % (P1 + 1);
-    double c[3] = {0, 0, 0}, sn_[3] = {0, 0, 0};
+    double c[SPC][3], sn_[SPC][3];
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp)
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp) c[sp][comp] = sn_[sp][comp] = 0.0;
     int idx = k;
     for (int m = 1; m <= p; ++m) {
       const double2 t = tw[idx];
 #pragma unroll
-      for (int comp = 0; comp < 3; ++comp) {
-        const double2 Um = reinterpret_cast<const double2*>(U)[(comp * P1 + j) * P1 + m];
-        c[comp] = fma(Um.x, t.x, c[comp]);
-        sn_[comp] = fma(Um.y, t.y, sn_[comp]);
+      for (int sp = 0; sp < SPC; ++sp) {
+        const double2* U2 = reinterpret_cast<const double2*>(Cp(sp));
+#pragma unroll
+        for (int comp = 0; comp < 3; ++comp) {
+          const double2 Um = U2[(comp * P1 + j) * P1 + m];
+          c[sp][comp] = fma(Um.x, t.x, c[sp][comp]);
+          sn_[sp][comp] = fma(Um.y, t.y, sn_[sp][comp]);
+        }
       }
       idx += k;
       if (idx >= nphi) idx -= nphi;
     }
     const double ct = tab[L.t + j], st = tab[L.st + j];
 #pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      if (side == 1 && (k == 0 || k == P1)) break;
-      const int kk = side ? nphi - k : k;
-      double v[3];
+    for (int sp = 0; sp < SPC; ++sp) {
+      if (!valid[sp]) continue;
+      const double* U = Cp(sp);
 #pragma unroll
-      for (int comp = 0; comp < 3; ++comp) {
-        const double U0 = U[2 * ((comp * P1 + j) * P1)];
-        v[comp] = fma(2.0, side ? c[comp] + sn_[comp] : c[comp] - sn_[comp], U0);
+      for (int side = 0; side < 2; ++side) {
+        if (side == 1 && (k == 0 || k == P1)) break;
+        const int kk = side ? nphi - k : k;
+        double v[3];
+#pragma unroll
+        for (int comp = 0; comp < 3; ++comp) {
+          const double U0 = U[2 * ((comp * P1 + j) * P1)];
+          v[comp] = fma(2.0, side ? c[sp][comp] + sn_[sp][comp] : c[sp][comp] - sn_[sp][comp], U0);
+        }
+        const double2 t = tw[kk];
+        const double cp = t.x, spn = t.y;
+        const int64_t i = sidx[sp] * nsn + j * nphi + kk;
+        double w0 = v[0] * st * cp + v[1] * ct * cp - v[2] * spn;
+        double w1 = v[0] * st * spn + v[1] * ct * spn + v[2] * cp;
+        double w2 = v[0] * ct - v[1] * st;
+        if (A.precond) {
+          w0 = fma(2.0, A.q[3 * i + 0], w0);
+          w1 = fma(2.0, A.q[3 * i + 1], w1);
+          w2 = fma(2.0, A.q[3 * i + 2], w2);
+        }
+        A.u[3 * i + 0] = w0;
+        A.u[3 * i + 1] = w1;
+        A.u[3 * i + 2] = w2;
       }
-      const double2 t = tw[kk];
-      const double cp = t.x, sp = t.y;
-      const int64_t i = s * nsn + j * nphi + kk;
-      double w0 = v[0] * st * cp + v[1] * ct * cp - v[2] * sp;
-      double w1 = v[0] * st * sp + v[1] * ct * sp + v[2] * cp;
-      double w2 = v[0] * ct - v[1] * st;
-      if (A.precond) {
-        w0 = fma(2.0, A.q[3 * i + 0], w0);
-        w1 = fma(2.0, A.q[3 * i + 1], w1);
-        w2 = fma(2.0, A.q[3 * i + 2], w2);
-      }
-      A.u[3 * i + 0] = w0;
-      A.u[3 * i + 1] = w1;
-      A.u[3 * i + 2] = w2;
     }
   }
 }
@@ -356,7 +427,37 @@ inline void launch_self(const SelfArgs& A, cudaStream_t s) {
       else k_self_t<128, 4><<<g, 128, smem, s>>>(A);
   }
 }
+// Two spheres per CTA (SPC = 2): independent work per thread for the scheduler
+// to interleave; same phases and barriers (measured against SPC = 1 in
+// profiles/r02_self_bench.jsonl).
+inline size_t self2_smem_bytes(int p) {
+  const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
+  return (size_t)(2 * (6 * nsn + 12 * P1 * P1) + 2 * nphi) * sizeof(double);
+}
+inline void launch_self2(const SelfArgs& A, cudaStream_t s) {
+  const size_t smem = self2_smem_bytes(A.p);
+  const unsigned g = (unsigned)((A.ns + 1) / 2);
+  switch (A.p) {
+    case 4: k_self_t<64, 8, 4, 2><<<g, 64, smem, s>>>(A); break;
+    case 6: k_self_t<64, 8, 6, 2><<<g, 64, smem, s>>>(A); break;
+    case 8: k_self_t<64, 8, 8, 2><<<g, 64, smem, s>>>(A); break;
+    case 12: k_self_t<128, 3, 12, 2><<<g, 128, smem, s>>>(A); break;
+    default:
+      if (A.p <= 8) k_self_t<64, 8, 0, 2><<<g, 64, smem, s>>>(A);
+      else k_self_t<128, 3, 0, 2><<<g, 128, smem, s>>>(A);
+  }
+}
+
 inline void set_self_smem(int p) {
+  const int smem2 = (int)self2_smem_bytes(p);
+  if (smem2 <= 227 * 1024) {
+    cudaFuncSetAttribute(k_self_t<64, 8, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(k_self_t<64, 8, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(k_self_t<64, 8, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(k_self_t<128, 3, 12, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(k_self_t<64, 8, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(k_self_t<128, 3, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+  }
   const int smem = (int)(self_smem_doubles(p) * sizeof(double));
   cudaFuncSetAttribute(k_self_t<64, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_self_t<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -90,7 +90,7 @@ def test_self_term_only(bie, oracle_mod, p, ns, poly, mu):
     _assert_parity(got, ref, f"self p={p}")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 13, 16, 17, 24, 32])
 def test_self_term_kernel_variants(bie, oracle_mod, p, variant):
     """Every self-term kernel (bie_set_self_kernel: 0 batched DMMA contractions,
