@@ -329,13 +329,16 @@ int bie_set_near_exclusion(bie_ctx* ctx, int mode);
 /*
  * Measurement knob: which kernel computes the spectral self term (rows a2,
  * a4-a6).  -1 (default): the fastest measured for the context's order (2 for
- * p <= 16, 0 above).  0: k_sht, the separable transforms as
+ * p <= 19, 0 above).  0: k_sht, the separable transforms as
  * small dense contractions on the FP64 tensor cores (mma.sync m8n8k4 f64,
  * SASS DMMA), one sphere per warp group; 1: the same schedule with DFMA
  * micro-kernels (compiled for p in {4, 6, 8, 12}; other orders use 0); 2: the
- * one-CTA-per-sphere scalar kernel.  All compute the same operator
- * (parity-tested); they differ only in schedule and speed.  NEXT-4's
- * coefficient accumulation always runs on k_sht.  BIE_ERR_ARG otherwise.
+ * one-CTA-per-sphere scalar kernel; 3: the same scalar kernel with two
+ * spheres per CTA (BIE_ERR_UNSUPPORTED, previous setting kept, when two
+ * spheres' staging exceeds 227 KB of shared memory, p >= 24).  All compute
+ * the same operator (parity-tested); they differ only in schedule and speed.
+ * NEXT-4's coefficient accumulation always runs on k_sht.  BIE_ERR_ARG
+ * outside -1..3.
  */
 int bie_set_self_kernel(bie_ctx* ctx, int variant);
 

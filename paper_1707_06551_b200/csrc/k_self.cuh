@@ -49,9 +49,10 @@ __host__ __device__ inline int64_t self_smem_doubles(int p) {
   const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
   const int64_t C = 6LL * nsn;       // spherical components; reused as ALPHA, then U
   const int64_t F = 12LL * P1 * P1;  // [2 dens][3 comp][j][m][re,im]; reused as PSI
+  // F first stages the sphere's f and q (6 nsn = 12 P1^2 doubles) for phase A.
   // PSI ([(n,m)][Y,G,X][re,im], 3 P1 (P1+1) <= F doubles) aliases F, dead after
-  // phase C: 24 P1^2 + 4 P1 doubles = 210 KB at p = 32 (<= 227 KB opt-in).
-  return C + F + 2LL * nphi;
+  // phase C: 24 P1^2 + 4 P1 + 2 doubles = 210 KB at p = 32 (<= 227 KB opt-in).
+  return C + F + 2LL * nphi + 2;  // + the staging mbarrier
 }
 
 // PT > 0: the order p is the compile-time constant PT (loop bounds, index
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   const int nlm = L.nlm;
   const int SZ = 6 * nsn + 12 * P1 * P1;  // per sphere: C [2][3][nsn] + F [2][3][P1][P1][2]
   double2* tw = reinterpret_cast<double2*>(sm + SPC * SZ);  // (cos, sin)(2 pi q/nphi), shared
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SPC * SZ + 2 * nphi);
   // per-sphere views: C; F (PSI aliases F, dead after phase C); U aliases C
   auto Cp = [&](int sp) { return sm + sp * SZ; };
   auto Fp_ = [&](int sp) { return sm + sp * SZ + 6 * nsn; };
@@ -88,7 +90,6 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   const double cS = 1.0 / (8.0 * kPi * A.mu), cD = 3.0 / (4.0 * kPi);
   const int tid = threadIdx.x, nt = blockDim.x;
 
-  for (int k = tid; k < nphi; k += nt) tw[k] = make_double2(tab[L.cph + k], tab[L.sph + k]);
   // ---------------------------------------------------------------- A (+ B0)
   // Node pairs (k, nphi-k) of a latitude are handled by one thread so that
   // the real-signal symmetry used by the DFT below is applied on the fly:
@@ -97,25 +98,13 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   const bool spec = A.self || A.alpha;
   auto node = [&](int sp, int j, int k, double* g) {
     const int kk = j * nphi + k;
-    const int64_t s = sidx[sp];
-    const int64_t i = s * nsn + kk;
-    const double a = ra[sp], aS = raS[sp];
-    double f0 = 0, f1 = 0, f2 = 0, q0 = 0, q1 = 0, q2 = 0;
-    if (A.f) { f0 = A.f[3 * i]; f1 = A.f[3 * i + 1]; f2 = A.f[3 * i + 2]; }
-    if (A.q) { q0 = A.q[3 * i]; q1 = A.q[3 * i + 1]; q2 = A.q[3 * i + 2]; }
+    const double aS = raS[sp];
+    const double* Fs = Fp_(sp);
+    const double f0 = Fs[3 * kk], f1 = Fs[3 * kk + 1], f2 = Fs[3 * kk + 2];
+    const double q0 = Fs[3 * nsn + 3 * kk], q1 = Fs[3 * nsn + 3 * kk + 1], q2 = Fs[3 * nsn + 3 * kk + 2];
     const double ct = tab[L.t + j], st = tab[L.st + j];
     const double cp = tw[k].x, sp_ = tw[k].y;
     const double n0 = st * cp, n1 = st * sp_, n2 = ct;
-    const double w = a * a * tab[L.wu + j];
-    // packed source record (row a2)
-    double2* r2 = reinterpret_cast<double2*>(A.rec + i * kRec);
-    const double ws = w * cS, wd = w * cD;
-    r2[0] = make_double2(rcx[sp] + a * n0, rcy[sp] + a * n1);
-    r2[1] = make_double2(rcz[sp] + a * n2, n0);
-    r2[2] = make_double2(n1, n2);
-    r2[3] = make_double2(ws * f0, ws * f1);
-    r2[4] = make_double2(ws * f2, wd * q0);
-    r2[5] = make_double2(wd * q1, wd * q2);
     // e_r = n, e_theta = (ct cp, ct sp, -st), e_phi = (-sp, cp, 0)
     g[0] = aS * (f0 * n0 + f1 * n1 + f2 * n2);
     g[1] = aS * (f0 * ct * cp + f1 * ct * sp_ - f2 * st);
@@ -124,17 +113,83 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     g[4] = q0 * ct * cp + q1 * ct * sp_ - q2 * st;
     g[5] = -q0 * sp_ + q1 * cp;
   };
-  __syncthreads();  // tw ready
+  // -------------------------------------------------------------- A0 staging
+  // f and q of the sphere (contiguous 24 nsn bytes each) land in F through the
+  // TMA unit (cp.async.bulk, no LSU wavefronts); the strided per-node reads of
+  // phase A and of the record writer then hit shared memory (ncu r18: the
+  // kernel was bound by L1 wavefronts, 84 %, half of them strided global
+  // accesses).  Unaligned user pointers fall back to cooperative loads.
+  const bool tma_f = A.f && !(reinterpret_cast<uintptr_t>(A.f) & 15);
+  const bool tma_q = A.q && !(reinterpret_cast<uintptr_t>(A.q) & 15);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  for (int k = tid; k < nphi; k += nt) tw[k] = make_double2(tab[L.cph + k], tab[L.sph + k]);
+#pragma unroll
+  for (int sp = 0; sp < SPC; ++sp) {
+    if (!valid[sp]) continue;
+    double* Fs = Fp_(sp);
+    for (int e = tid; e < 3 * nsn; e += nt) {
+      if (!tma_f) Fs[e] = A.f ? A.f[sidx[sp] * 3 * nsn + e] : 0.0;
+      if (!tma_q) Fs[3 * nsn + e] = A.q ? A.q[sidx[sp] * 3 * nsn + e] : 0.0;
+    }
+  }
+  __syncthreads();  // tw, fallback staging and the mbarrier ready
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)(3 * nsn * sizeof(double));
+    int nvalid = 0;
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp) nvalid += valid[sp] ? 1 : 0;
+    mbar_arrive_expect_tx(bar, (uint32_t)nvalid * bytes * ((tma_f ? 1 : 0) + (tma_q ? 1 : 0)));
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp) {
+      if (!valid[sp]) continue;
+      if (tma_f) bulk_g2s(Fp_(sp), A.f + sidx[sp] * 3 * nsn, bytes, bar);
+      if (tma_q) bulk_g2s(Fp_(sp) + 3 * nsn, A.q + sidx[sp] * 3 * nsn, bytes, bar);
+    }
+  }
+  mbar_wait(bar, 0);
+  // -------------------------------------------------------------- A1 records
+  // Packed source records (row a2), written as consecutive 16-byte chunks so
+  // that a warp's stores cover contiguous 512 bytes.
+#pragma unroll
+  for (int sp = 0; sp < SPC; ++sp) {
+    if (!valid[sp]) continue;
+    const double* Fs = Fp_(sp);
+    const double a = ra[sp];
+    double2* out = reinterpret_cast<double2*>(A.rec + sidx[sp] * nsn * kRec);
+    for (int e = tid; e < 6 * nsn; e += nt) {
+      const int kk = e / 6, part = e - 6 * kk;
+      const int j = kk / nphi, k = kk - j * nphi;
+      double2 v;
+      if (part < 3) {
+        const double st = tab[L.st + j];
+        const double2 t = tw[k];
+        const double n0 = st * t.x, n1 = st * t.y, n2 = tab[L.t + j];
+        v = part == 0 ? make_double2(rcx[sp] + a * n0, rcy[sp] + a * n1)
+                      : (part == 1 ? make_double2(rcz[sp] + a * n2, n0) : make_double2(n1, n2));
+      } else {
+        const double w = a * a * tab[L.wu + j];
+        // (f0 f1 | f2 q0 | q1 q2) scaled by (ws ws | ws wd | wd wd)
+        const int u0 = 2 * (part - 3), u1 = u0 + 1;
+        const double x0 = Fs[u0 < 3 ? 3 * kk + u0 : 3 * nsn + 3 * kk + u0 - 3];
+        const double x1 = Fs[u1 < 3 ? 3 * kk + u1 : 3 * nsn + 3 * kk + u1 - 3];
+        v = make_double2(x0 * w * (u0 < 3 ? cS : cD), x1 * w * (u1 < 3 ? cS : cD));
+      }
+      out[e] = v;
+    }
+  }
   for (int it = tid; it < P1 * (P1 + 1); it += nt) {
     const int j = it / (P1 + 1), k = it - j * (P1 + 1);
     const bool pair = k > 0 && k < P1;
 #pragma unroll
     for (int sp = 0; sp < SPC; ++sp) {
       if (!valid[sp]) continue;
-      double g1[6], g2[6];
-      node(sp, j, k, g1);
-      if (pair) node(sp, j, nphi - k, g2);
       if (spec) {
+        double g1[6], g2[6];
+        node(sp, j, k, g1);
+        if (pair) node(sp, j, nphi - k, g2);
         double* row = Cp(sp) + j * nphi;
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
@@ -176,18 +231,19 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
         double* F = Fp_(sp);
         double re1 = (m1 & 1) ? g[0] - g[P1] : g[0] + g[P1], im1 = 0.0;
         double re2 = (m2 & 1) ? g[0] - g[P1] : g[0] + g[P1], im2 = 0.0;
-        int i1 = m1, i2 = two ? m2 : 0;
+        // (cos, sin)(m phi_k) by the angle-addition recurrence from
+        // (cos, sin)(m phi_1): no twiddle loads in the loop (rounding grows
+        // like k eps, < 1e-14 at p = 32)
+        const double2 w1 = tw[m1], w2 = tw[two ? m2 : 0];
+        double2 t1 = w1, t2 = w2;
         for (int k = 1; k <= p; ++k) {
           const double gs = g[k], gd = g[nphi - k];
-          const double2 t1 = tw[i1], t2 = tw[i2];
           re1 = fma(gs, t1.x, re1);
           im1 = fma(-gd, t1.y, im1);
           re2 = fma(gs, t2.x, re2);
           im2 = fma(-gd, t2.y, im2);
-          i1 += m1;
-          if (i1 >= nphi) i1 -= nphi;
-          i2 += m2;
-          if (i2 >= nphi) i2 -= nphi;
+          t1 = make_double2(fma(t1.x, w1.x, -t1.y * w1.y), fma(t1.y, w1.x, t1.x * w1.y));
+          t2 = make_double2(fma(t2.x, w2.x, -t2.y * w2.y), fma(t2.y, w2.x, t2.x * w2.y));
         }
         F[2 * (row * P1 + m1)] = re1;
         F[2 * (row * P1 + m1) + 1] = im1;
@@ -360,9 +416,9 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     for (int sp = 0; sp < SPC; ++sp)
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp) c[sp][comp] = sn_[sp][comp] = 0.0;
-    int idx = k;
+    const double2 wk = tw[k];  // (cos, sin)(m phi_k) by angle addition in m
+    double2 t = wk;
     for (int m = 1; m <= p; ++m) {
-      const double2 t = tw[idx];
 #pragma unroll
       for (int sp = 0; sp < SPC; ++sp) {
         const double2* U2 = reinterpret_cast<const double2*>(Cp(sp));
@@ -373,8 +429,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
           sn_[sp][comp] = fma(Um.y, t.y, sn_[sp][comp]);
         }
       }
-      idx += k;
-      if (idx >= nphi) idx -= nphi;
+      t = make_double2(fma(t.x, wk.x, -t.y * wk.y), fma(t.y, wk.x, t.x * wk.y));
     }
     const double ct = tab[L.t + j], st = tab[L.st + j];
 #pragma unroll
@@ -410,18 +465,19 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   }
 }
 
-// Launch configurations chosen by tools/self_tune.cu (profiles/r01_self_tune.txt):
-// small spheres (p <= 8) prefer many 64-thread CTAs, larger ones 128 threads.
+// Launch configurations chosen by tools/self_tune.cu (profiles/r01_self_tune.txt,
+// re-swept after the TMA staging in profiles/r02_self_tune.jsonl): p <= 6 many
+// 64-thread CTAs (64 registers, 16 per SM), p = 8 and 12 128 threads.
 // The orders of the BASELINE configurations (4, 6, 8, 12) get compile-time-p
 // instantiations; every other p runs the generic kernel.
 inline void launch_self(const SelfArgs& A, cudaStream_t s) {
   const size_t smem = self_smem_doubles(A.p) * sizeof(double);
   const unsigned g = (unsigned)A.ns;
   switch (A.p) {
-    case 4: k_self_t<64, 12, 4><<<g, 64, smem, s>>>(A); break;
-    case 6: k_self_t<64, 12, 6><<<g, 64, smem, s>>>(A); break;
-    case 8: k_self_t<64, 12, 8><<<g, 64, smem, s>>>(A); break;
-    case 12: k_self_t<128, 4, 12><<<g, 128, smem, s>>>(A); break;
+    case 4: k_self_t<64, 16, 4><<<g, 64, smem, s>>>(A); break;
+    case 6: k_self_t<64, 16, 6><<<g, 64, smem, s>>>(A); break;
+    case 8: k_self_t<128, 6, 8><<<g, 128, smem, s>>>(A); break;
+    case 12: k_self_t<128, 5, 12><<<g, 128, smem, s>>>(A); break;
     default:
       if (A.p <= 8) k_self_t<64, 12><<<g, 64, smem, s>>>(A);
       else k_self_t<128, 4><<<g, 128, smem, s>>>(A);
@@ -432,7 +488,7 @@ inline void launch_self(const SelfArgs& A, cudaStream_t s) {
 // profiles/r02_self_bench.jsonl).
 inline size_t self2_smem_bytes(int p) {
   const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
-  return (size_t)(2 * (6 * nsn + 12 * P1 * P1) + 2 * nphi) * sizeof(double);
+  return (size_t)(2 * (6 * nsn + 12 * P1 * P1) + 2 * nphi + 2) * sizeof(double);
 }
 inline void launch_self2(const SelfArgs& A, cudaStream_t s) {
   const size_t smem = self2_smem_bytes(A.p);
@@ -461,10 +517,10 @@ inline void set_self_smem(int p) {
   const int smem = (int)(self_smem_doubles(p) * sizeof(double));
   cudaFuncSetAttribute(k_self_t<64, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_self_t<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<64, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<64, 12, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<64, 12, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<128, 4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<128, 6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<128, 5, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 // Source packing alone (row a2) for the off-surface evaluator; also writes

@@ -94,11 +94,21 @@ def test_self_term_only(bie, oracle_mod, p, ns, poly, mu):
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 13, 16, 17, 24, 32])
 def test_self_term_kernel_variants(bie, oracle_mod, p, variant):
     """Every self-term kernel (bie_set_self_kernel: 0 batched DMMA contractions,
-    1 batched DFMA, 2 round-1 per-sphere) on 5 polydisperse spheres -- a
+    1 batched DFMA, 2 round-1 per-sphere, 3 per-sphere with two spheres per CTA) on 5 polydisperse spheres -- a
     ragged last batch for the 4- and 2-sphere batches of k_sht -- against the
     oracle's direct projection (O-4), S and D together and each alone."""
     c, a, f, q, mu = _random_case(700 + p, 5, p, True, 0.9)
     ctx = bie.bie_create(c, a, p, mu)
+    P1, nphi = p + 1, 2 * p + 2
+    two_sphere_smem = (2 * (6 * P1 * nphi + 12 * P1 * P1) + 2 * nphi) * 8
+    if variant == 3 and two_sphere_smem > 227 * 1024:
+        # include/bie.h: variant 3 stages two spheres per CTA; beyond 227 KB it
+        # is refused with BIE_ERR_UNSUPPORTED and the previous kernel stays.
+        with pytest.raises(bie.BieError) as e:
+            bie.bie_set_self_kernel(ctx, variant)
+        assert e.value.status == bie.BIE_ERR_UNSUPPORTED
+        ctx.close()
+        return
     bie.bie_set_self_kernel(ctx, variant)
     N = bie.bie_num_nodes(ctx)
     for fx, qx, what in ((f, q, "S+D"), (f, None, "S"), (None, q, "D")):

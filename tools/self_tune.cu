@@ -9,21 +9,24 @@
 
 using namespace bie;
 
-template <int TPB, int MINB, int PT = 0>
+static char* g_flush = nullptr;  // 256 MB written before every timed launch (L2 flush)
+
+template <int TPB, int MINB, int PT = 0, int SPC = 1>
 void run(const char* name, SelfArgs A, int64_t N) {
-  const size_t smem = self_smem_doubles(A.p) * sizeof(double);
-  cudaFuncSetAttribute(k_self_t<TPB, MINB, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = SPC == 1 ? self_smem_doubles(A.p) * sizeof(double) : self2_smem_bytes(A.p);
+  cudaFuncSetAttribute(k_self_t<TPB, MINB, PT, SPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_self_t<TPB, MINB, PT>, TPB, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_self_t<TPB, MINB, PT, SPC>, TPB, smem);
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, k_self_t<TPB, MINB, PT>);
+  cudaFuncGetAttributes(&fa, k_self_t<TPB, MINB, PT, SPC>);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
   for (int r = 0; r < 12; ++r) {
+    cudaMemsetAsync(g_flush, r, 256u << 20);
     cudaEventRecord(e0);
-    k_self_t<TPB, MINB, PT><<<(unsigned)A.ns, TPB, smem>>>(A);
+    k_self_t<TPB, MINB, PT, SPC><<<(unsigned)((A.ns + SPC - 1) / SPC), TPB, smem>>>(A);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -36,8 +39,9 @@ void run(const char* name, SelfArgs A, int64_t N) {
 }
 
 int main() {
-  for (int p : {6, 12}) {
-    const int64_t ns = p == 6 ? 10000 : 4096;
+  cudaMalloc(&g_flush, 256u << 20);
+  for (int p : {6, 8, 12}) {
+    const int64_t ns = p == 6 ? 10000 : (p == 8 ? 1000 : 4096);
     const int nsn = (p + 1) * (2 * p + 2);
     const int64_t N = ns * nsn;
     const TableLayout L(p);
@@ -68,14 +72,28 @@ int main() {
     run<128, 4>("T128 minB4 generic", A, N);
     if (p == 6) {
       run<64, 12, 6>("T64 minB12 PT=6", A, N);
+      run<64, 16, 6>("T64 minB16 PT=6", A, N);
+      run<64, 8, 6, 2>("T64 minB8 PT=6 SPC2", A, N);
+      run<64, 10, 6, 2>("T64 minB10 PT=6 SPC2", A, N);
       run<128, 6, 6>("T128 minB6 PT=6", A, N);
-      run<64, 8, 6>("T64 minB8 PT=6", A, N);
+      run<128, 8, 6>("T128 minB8 PT=6", A, N);
       run<32, 16, 6>("T32 minB16 PT=6", A, N);
+      run<32, 24, 6>("T32 minB24 PT=6", A, N);
+      run<32, 32, 6>("T32 minB32 PT=6", A, N);
+    } else if (p == 8) {
+      run<64, 12, 8>("T64 minB12 PT=8", A, N);
+      run<64, 16, 8>("T64 minB16 PT=8", A, N);
+      run<64, 8, 8, 2>("T64 minB8 PT=8 SPC2", A, N);
+      run<128, 6, 8>("T128 minB6 PT=8", A, N);
+      run<32, 24, 8>("T32 minB24 PT=8", A, N);
     } else {
       run<128, 4, 12>("T128 minB4 PT=12", A, N);
+      run<128, 5, 12>("T128 minB5 PT=12", A, N);
       run<128, 6, 12>("T128 minB6 PT=12", A, N);
+      run<128, 3, 12, 2>("T128 minB3 PT=12 SPC2", A, N);
       run<256, 3, 12>("T256 minB3 PT=12", A, N);
       run<64, 8, 12>("T64 minB8 PT=12", A, N);
+      run<64, 10, 12>("T64 minB10 PT=12", A, N);
     }
     cudaFree(tab); cudaFree(cen); cudaFree(rad); cudaFree(f); cudaFree(q); cudaFree(u); cudaFree(rec);
   }
