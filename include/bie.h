@@ -317,6 +317,18 @@ int bie_solve_porous(bie_ctx* ctx, const double* uinf, double* mu, double tol, i
 int bie_set_near_mode(bie_ctx* ctx, int mode);
 
 /*
+ * Measurement knob: schedule of the off-surface near correction (NEXT-1 in
+ * bie_eval_offsurface / bie_eval_traction).  0 (default): the (target, near
+ * sphere) pairs grouped by sphere, one CTA per sphere chunk with the sphere's
+ * records in shared memory, per-pair results summed per target in ascending
+ * sphere order; costs one stream synchronisation per call (the pair count
+ * sizes the scratch).  1: one thread per Morton-sorted target walking its own
+ * near spheres (round-2 schedule).  Same operator (parity-tested).
+ * BIE_ERR_ARG outside 0..1.
+ */
+int bie_set_near_off_schedule(bie_ctx* ctx, int schedule);
+
+/*
  * How the applies treat the smooth rule of near pairs: 1 the far-field kernel
  * skips them (the correction adds the exact field only); 0 the far field keeps
  * them and the correction subtracts them pointwise; -1 (default) the cheaper

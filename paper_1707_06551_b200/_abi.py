@@ -23,7 +23,7 @@ SYMBOLS = (
     "bie_get_nodes", "bie_apply_SLDL", "bie_apply_SL", "bie_apply_DL", "bie_apply_parts",
     "bie_eval_offsurface", "bie_apply_SLDL_host", "bie_eval_offsurface_host",
     "bie_set_profiling", "bie_get_profile", "bie_reset_profile", "bie_set_source_chunks",
-    "bie_set_self_kernel", "bie_set_near_mode", "bie_set_near_exclusion", "bie_set_far_reduction",
+    "bie_set_self_kernel", "bie_set_near_mode", "bie_set_near_exclusion", "bie_set_near_off_schedule", "bie_set_far_reduction",
     "bie_near_lists",
     "bie_set_near", "bie_near_pairs", "bie_solve_porous", "bie_apply_K", "bie_eval_traction",
     "bie_status_string", "bie_last_error",
@@ -58,6 +58,7 @@ _lib.bie_reset_profile.argtypes = [_vp]
 _lib.bie_set_source_chunks.argtypes = [_vp, _i32]
 _lib.bie_set_self_kernel.argtypes = [_vp, _i32]
 _lib.bie_set_near_mode.argtypes = [_vp, _i32]
+_lib.bie_set_near_off_schedule.argtypes = [_vp, _i32]
 _lib.bie_set_near_exclusion.argtypes = [_vp, _i32]
 _lib.bie_near_lists.argtypes = [_vp, _vp, _i64, _d, _vp, _vp, _i64, ctypes.POINTER(_i64)]
 _lib.bie_set_far_reduction.argtypes = [_vp, _i32]
@@ -313,6 +314,12 @@ def bie_near_lists(centres, radii, eta: float):
 def bie_set_near_exclusion(ctx, mode: int):
     """Near pairs in the far field: 1 skipped, 0 subtracted, -1 auto (include/bie.h)."""
     _check(ctx, _lib.bie_set_near_exclusion(ctx.handle, int(mode)))
+
+
+def bie_set_near_off_schedule(ctx, schedule: int):
+    """Off-surface near correction schedule: 0 pairs grouped by sphere (default),
+    1 one thread per Morton-sorted target (include/bie.h)."""
+    _check(ctx, _lib.bie_set_near_off_schedule(ctx.handle, int(schedule)))
 
 
 def bie_set_near_mode(ctx, mode: int):

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "../../include/bie.h"
 #include "common.cuh"
@@ -107,6 +108,13 @@ struct bie_ctx {
   // Morton-sorted target order scratch (off-surface near correction)
   void* d_sort = nullptr;
   size_t sort_cap = 0;
+  // off-surface near correction schedule (bie_set_near_off_schedule): 0 pairs
+  // grouped by sphere (default), 1 one thread per Morton-sorted target
+  int noff_sched = 0;
+  void* d_grp1 = nullptr;  // per-target scratch of the grouped schedule
+  size_t grp1_cap = 0;
+  void* d_grp2 = nullptr;  // per-pair / per-sphere scratch
+  size_t grp2_cap = 0;
   // NEXT-4 (bie_set_near_mode): 0 direct, 1 rotated (PAPER §4.2), 2/3 measurement
   int near_mode = 0;
   int near_excl = -1;  // bie_set_near_exclusion: -1 auto (cost model), 0 subtract, 1 exclude
@@ -443,6 +451,138 @@ static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K, int part = 0)
 
 // Near correction at m arbitrary targets: velocity (+ pressure when p) or,
 // with target normals tn, traction (K).  Accumulates onto u (and p).
+// Carves 256-byte-aligned arrays out of one scratch buffer (base == nullptr:
+// sizing pass).
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    T* r = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return r;
+  }
+};
+
+static int grow(bie_ctx* c, void** buf, size_t* cap, size_t need, const char* what) {
+  if (need <= *cap) return BIE_OK;
+  cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  if (cudaMalloc(buf, need) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, BIE_ERR_ALLOC, "%s scratch", what);
+  }
+  *cap = need;
+  return BIE_OK;
+}
+
+// Grouped schedule of the off-surface near correction (k_near.cuh): pairs
+// (target, near sphere) listed per target, grouped by sphere with a stable
+// radix sort, evaluated one CTA per (sphere, chunk), summed per target.  One
+// stream synchronisation reads the pair count (it sizes the pair arrays).
+static int run_near_off_grp(bie_ctx* c, NearOffArgs NO, cudaStream_t s) {
+  const int64_t m = NO.M, ns = c->ns;
+  NearGrp G{};
+  // per-target arrays and the scan of the counts
+  size_t scan_tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (const int*)nullptr, (int*)nullptr, (int)(m + 1), s);
+  auto carve1 = [&](char* base, size_t* total) {
+    Carve cv{base};
+    G.cnt = cv.take<int>(m + 1);
+    G.off = cv.take<int>(m + 1);
+    void* tmp = cv.take<char>(scan_tmp);
+    *total = cv.off;
+    return tmp;
+  };
+  size_t need1 = 0;
+  carve1(nullptr, &need1);
+  int rc = grow(c, &c->d_grp1, &c->grp1_cap, need1, "near pair count");
+  if (rc) return rc;
+  void* scan1 = carve1(static_cast<char*>(c->d_grp1), &need1);
+  Ev ev;
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  cudaMemsetAsync(G.cnt + m, 0, sizeof(int), s);
+  const unsigned gt = (unsigned)((m + 127) / 128);
+  k_noff_pairs<false><<<gt, 128, 0, s>>>(NO, G);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(scan1, scan_tmp, G.cnt, const_cast<int*>(G.off), (int)(m + 1), s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "near pair scan");
+  int P = 0;
+  e = cudaMemcpyAsync(&P, G.off + m, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "near pair count");
+  prof_end(c, s, &ev);
+  c->launches[BIE_KIND_NEAR] += 2;  // k_noff_pairs + the scan's two kernels (one counted)
+  if (P == 0) return BIE_OK;
+  // per-pair and per-sphere arrays
+  int bits = 1;
+  while (bits < 31 && (1LL << bits) <= ns) ++bits;
+  size_t sort_tmp = 0, sscan_tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const int*)nullptr, (int*)nullptr, (const int*)nullptr,
+                                  (int*)nullptr, P, 0, bits, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, sscan_tmp, (const int*)nullptr, (int*)nullptr, (int)(ns + 1), s);
+  int* sorted_s = nullptr;
+  void *stmp = nullptr, *sctmp = nullptr;
+  auto carve2 = [&](char* base) {
+    Carve cv{base};
+    G.pair_s = cv.take<int>(P);
+    G.pair_t = cv.take<int>(P);
+    G.pair_j = cv.take<int>(P);
+    sorted_s = cv.take<int>(P);
+    G.sorted_j = cv.take<int>(P);
+    G.res = cv.take<double>(4 * (size_t)P);
+    G.scount = cv.take<int>(ns + 1);
+    G.nch = cv.take<int>(ns + 1);
+    G.sfirst = cv.take<int>(ns + 1);
+    G.choff = cv.take<int>(ns + 1);
+    stmp = cv.take<char>(sort_tmp);
+    sctmp = cv.take<char>(sscan_tmp);
+    return cv.off;
+  };
+  if ((rc = grow(c, &c->d_grp2, &c->grp2_cap, carve2(nullptr), "near pair"))) return rc;
+  carve2(static_cast<char*>(c->d_grp2));
+  prof_begin(c, BIE_KIND_NEAR, s, &ev);
+  cudaMemsetAsync(G.scount, 0, (ns + 1) * sizeof(int), s);
+  cudaMemsetAsync(G.nch, 0, (ns + 1) * sizeof(int), s);
+  k_noff_pairs<true><<<gt, 128, 0, s>>>(NO, G);
+  e = cub::DeviceRadixSort::SortPairs(stmp, sort_tmp, G.pair_s, sorted_s, G.pair_j, const_cast<int*>(G.sorted_j),
+                                      P, 0, bits, s);
+  if (e == cudaSuccess) {
+    k_noff_nch<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(ns, G.scount, G.nch);
+    e = cub::DeviceScan::ExclusiveSum(sctmp, sscan_tmp, G.scount, const_cast<int*>(G.sfirst), (int)(ns + 1), s);
+  }
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::ExclusiveSum(sctmp, sscan_tmp, G.nch, const_cast<int*>(G.choff), (int)(ns + 1), s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "near pair grouping");
+  // chunks <= P / kGrpChunk + (spheres with pairs) <= P / kGrpChunk + min(ns, P)
+  const unsigned gb = (unsigned)((P + kGrpChunk - 1) / kGrpChunk + std::min<int64_t>(ns, P));
+  const bool stage = noff_grp_stage(c->p);
+  const size_t sm = noff_grp_smem_doubles(c->p, stage) * sizeof(double);
+  const bool K = NO.tn != nullptr, pr = !K && NO.pres;
+#define NOFF_GRP(PR, KK)                                                                       \
+  do {                                                                                         \
+    if (stage) {                                                                               \
+      cudaFuncSetAttribute(k_noff_grp<PR, KK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+      k_noff_grp<PR, KK, true><<<gb, kGrpChunk, sm, s>>>(NO, G);                               \
+    } else {                                                                                   \
+      cudaFuncSetAttribute(k_noff_grp<PR, KK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+      k_noff_grp<PR, KK, false><<<gb, kGrpChunk, sm, s>>>(NO, G);                              \
+    }                                                                                          \
+  } while (0)
+  if (K) NOFF_GRP(false, true);
+  else if (pr) NOFF_GRP(true, false);
+  else NOFF_GRP(false, false);
+#undef NOFF_GRP
+  if (pr) k_noff_sum<true><<<gt, 128, 0, s>>>(NO, G);
+  else k_noff_sum<false><<<gt, 128, 0, s>>>(NO, G);
+  prof_end(c, s, &ev);
+  // k_noff_pairs, radix sort (histogram, scan, 2 onesweep passes for <= 16 key
+  // bits), k_noff_nch, two scans (2 kernels each), k_noff_grp, k_noff_sum
+  c->launches[BIE_KIND_NEAR] += 11 + (bits > 16 ? 2 : 0);
+  return launch_check(c, K ? "k_noff_grp<K>" : "k_noff_grp");
+}
+
 static int run_near_off(bie_ctx* c, const double* tg, const double* tn, int64_t m, double* u,
                         double* p, cudaStream_t s) {
   NearOffArgs NO;
@@ -471,6 +611,7 @@ static int run_near_off(bie_ctx* c, const double* tg, const double* tn, int64_t 
   NO.gnx = c->gn[0];
   NO.gny = c->gn[1];
   NO.gnz = c->gn[2];
+  if (c->noff_sched == 0 && m < (int64_t)INT32_MAX) return run_near_off_grp(c, NO, s);
   // process the targets in Morton order of their grid cell: neighbouring lanes
   // then share near spheres (coefficients and records hit L1 instead of L2)
   if (m <= (int64_t)INT32_MAX) {
@@ -955,6 +1096,8 @@ void bie_destroy(bie_ctx* c) {
   cudaFree(c->d_cell_start);
   cudaFree(c->d_cell_items);
   cudaFree(c->d_sort);
+  cudaFree(c->d_grp1);
+  cudaFree(c->d_grp2);
   delete c;
 }
 
@@ -1488,6 +1631,13 @@ int bie_set_near_exclusion(bie_ctx* c, int mode) {
   if (!c) return BIE_ERR_ARG;
   if (mode < -1 || mode > 1) return fail(c, BIE_ERR_ARG, "near exclusion must be -1, 0 or 1%s");
   c->near_excl = mode;
+  return BIE_OK;
+}
+
+int bie_set_near_off_schedule(bie_ctx* c, int schedule) {
+  if (!c) return BIE_ERR_ARG;
+  if (schedule < 0 || schedule > 1) return fail(c, BIE_ERR_ARG, "near off-surface schedule must be 0 or 1%s");
+  c->noff_sched = schedule;
   return BIE_OK;
 }
 

@@ -414,4 +414,189 @@ __global__ void __launch_bounds__(128) k_near_off(const NearOffArgs A) {
   if (PRESSURE && A.pres) A.pres[t] += dp;
 }
 
+// ------------------------------------------- grouped schedule (default)
+// The (target, near sphere) pairs of the off-surface correction grouped by
+// sphere: one CTA takes up to kGrpChunk pairs of ONE sphere, whose records,
+// qn3 and expansion coefficients are staged in shared memory once and read as
+// broadcasts by every thread.  (The per-target schedule above makes each lane
+// walk its own spheres' records through L1/L2: 33 % FP64 pipe, bound by long
+// scoreboard stalls, profiles/r02_ncu_nearoff_cfg5.txt.)  Per-pair results go
+// to a buffer; k_noff_sum adds them per target in ascending sphere order, so
+// the result is deterministic and does not depend on the grouping.
+constexpr int kGrpChunk = 128;
+
+struct NearGrp {
+  int* cnt;              // [M + 1] near spheres per target (count pass; cnt[M] = 0)
+  const int* off;        // [M + 1] exclusive scan of cnt: pair range of each target
+  int* pair_s;           // [P] sphere of pair j (target-major, ascending sphere in a target)
+  int* pair_t;           // [P] target of pair j
+  int* pair_j;           // [P] j (the values of the sphere sort)
+  int* scount;           // [ns + 1] pairs per sphere (integer atomics: order-free)
+  int* nch;              // [ns + 1] chunks per sphere
+  const int* sorted_j;   // [P] pair indices grouped by sphere (stable: ascending target)
+  const int* sfirst;     // [ns + 1] exclusive scan of scount
+  const int* choff;      // [ns + 1] exclusive scan of nch
+  double* res;           // [P][4] (du, dp) of each pair
+};
+
+// Near spheres of target x in the candidate order of k_near_off (27 cells).
+template <typename F>
+__device__ __forceinline__ void near_candidates(const NearOffArgs& A, const double* x, F&& take) {
+  auto cell = [&](double v, double o, int n) {
+    const double c = floor((v - o) / A.gh);
+    return (int)(c < 0 ? 0 : (c > n - 1 ? n - 1 : c));
+  };
+  const int cx = cell(x[0], A.g0x, A.gnx), cy = cell(x[1], A.g0y, A.gny), cz = cell(x[2], A.g0z, A.gnz);
+  for (int iz = max(cz - 1, 0); iz <= min(cz + 1, A.gnz - 1); ++iz)
+    for (int iy = max(cy - 1, 0); iy <= min(cy + 1, A.gny - 1); ++iy)
+      for (int ix = max(cx - 1, 0); ix <= min(cx + 1, A.gnx - 1); ++ix) {
+        const int cid = (iz * A.gny + iy) * A.gnx + ix;
+        for (int q = A.cell_start[cid]; q < A.cell_start[cid + 1]; ++q) {
+          const int sidx = A.cell_items[q];
+          const double dx = __dsub_rn(x[0], A.centres[3 * sidx]), dy = __dsub_rn(x[1], A.centres[3 * sidx + 1]),
+                       dz = __dsub_rn(x[2], A.centres[3 * sidx + 2]);
+          const double a = A.radii[sidx];
+          const double r =
+              __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+          const double dsurf = __dsub_rn(r, a);
+          if (dsurf >= 0.0 && dsurf < __dmul_rn(A.eta, __dmul_rn(2.0, a))) take(sidx);  // exterior only
+        }
+      }
+}
+
+// WRITE = false: cnt[t] = number of near spheres of target t.  WRITE = true:
+// the pairs of t at off[t].. in ascending sphere order, and the per-sphere counts.
+template <bool WRITE>
+__global__ void __launch_bounds__(128) k_noff_pairs(const NearOffArgs A, const NearGrp G) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= A.M) return;
+  const double x[3] = {A.tx[3 * t], A.tx[3 * t + 1], A.tx[3 * t + 2]};
+  const int base = WRITE ? G.off[t] : 0;
+  int r = 0;
+  near_candidates(A, x, [&](int sidx) {
+    if (WRITE) G.pair_s[base + r] = sidx;
+    ++r;
+  });
+  if (!WRITE) {
+    G.cnt[t] = r;
+    return;
+  }
+  int* ps = G.pair_s + base;
+  for (int i = 1; i < r; ++i) {  // a handful of spheres: insertion sort
+    const int v = ps[i];
+    int j = i - 1;
+    while (j >= 0 && ps[j] > v) { ps[j + 1] = ps[j]; --j; }
+    ps[j + 1] = v;
+  }
+  for (int i = 0; i < r; ++i) {
+    G.pair_t[base + i] = (int)t;
+    G.pair_j[base + i] = base + i;
+    atomicAdd(&G.scount[ps[i]], 1);
+  }
+}
+
+__global__ void k_noff_nch(int64_t ns, const int* __restrict__ scount, int* __restrict__ nch) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < ns) nch[s] = (scount[s] + kGrpChunk - 1) / kGrpChunk;
+}
+
+__host__ __device__ inline int64_t noff_grp_smem_doubles(int p, bool stage) {
+  const int nlm = (p + 1) * (p + 2) / 2, nsn = (p + 1) * (2 * p + 2);
+  const int64_t head = (3LL * nlm + 10LL * nlm + 1) & ~1LL;  // rA rB rC, coefficients
+  return head + (stage ? 12LL * nsn + nsn : 0);
+}
+__host__ __device__ inline bool noff_grp_stage(int p) { return noff_grp_smem_doubles(p, true) * 8 <= 100 * 1024; }
+
+// One CTA per (sphere, chunk of <= kGrpChunk of its pairs); thread i takes one
+// pair.  STAGE: the sphere's packed records and qn3 in shared memory (else
+// read with warp-uniform addresses, which L1 serves as broadcasts).
+template <bool PRESSURE, bool K, bool STAGE>
+__global__ void __launch_bounds__(kGrpChunk) k_noff_grp(const NearOffArgs A, const NearGrp G) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  const int ns = (int)A.ns;
+  if (b >= G.choff[ns]) return;
+  int lo = 0, hi = ns;  // largest s with choff[s] <= b
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (G.choff[mid] <= b) lo = mid;
+    else hi = mid;
+  }
+  const int s = lo;
+  const int i0 = G.sfirst[s] + (b - G.choff[s]) * kGrpChunk;
+  const int i1 = min(i0 + kGrpChunk, G.sfirst[s + 1]);
+  const int p = A.p, nsn = A.nsn;
+  const TableLayout L(p);
+  const int nlm = L.nlm;
+  double* rt = sm;              // rA, rB, rC [3][nlm]
+  double* cf = rt + 3 * nlm;    // [nlm][10]
+  double* srec = sm + ((13 * nlm + 1) & ~1);  // STAGE: [nsn][12], then qn3 [nsn]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 3 * nlm; e += kGrpChunk) rt[e] = A.tab[L.rA + e];
+  const double* gcf = A.coef + (int64_t)s * nlm * 10;
+  for (int e = tid; e < 10 * nlm; e += kGrpChunk) cf[e] = gcf[e];
+  const double2* sr = reinterpret_cast<const double2*>(A.rec + (int64_t)s * nsn * kRec);
+  const double* sq = (PRESSURE && !K) ? A.qn3 + (int64_t)s * nsn : nullptr;
+  if (STAGE) {
+    double2* s2 = reinterpret_cast<double2*>(srec);
+    for (int e = tid; e < 6 * nsn; e += kGrpChunk) s2[e] = sr[e];
+    if (PRESSURE && !K)
+      for (int e = tid; e < nsn; e += kGrpChunk) srec[12 * nsn + e] = sq[e];
+    sr = s2;
+    if (PRESSURE && !K) sq = srec + 12 * nsn;
+  }
+  __syncthreads();
+  const int i = i0 + tid;
+  if (i >= i1) return;
+  const int j = G.sorted_j[i];
+  const int t = G.pair_t[j];
+  const double x[3] = {A.tx[3 * (int64_t)t], A.tx[3 * (int64_t)t + 1], A.tx[3 * (int64_t)t + 2]};
+  const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+  const double a = A.radii[s];
+  double ex[3], pe = 0.0, acc[3] = {0.0, 0.0, 0.0}, pacc = 0.0;
+  if constexpr (K) {
+    const double nv[3] = {A.tn[3 * (int64_t)t], A.tn[3 * (int64_t)t + 1], A.tn[3 * (int64_t)t + 2]};
+    exterior_traction(p, cf, rt, rt + nlm, cs, a, x, nv, ex);
+    for (int k = 0; k < nsn; ++k) {
+      const double2* q2 = sr + k * (kRec / 2);
+      pair_K<false>(q2[0], q2[1], q2[4], q2[5], x, nv, acc, 0, 0, 1);
+    }
+  } else {
+    exterior_field<PRESSURE>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, x, ex, &pe);
+    for (int k = 0; k < nsn; ++k) {
+      const double2* q2 = sr + k * (kRec / 2);
+      pair_acc<false, PRESSURE>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], PRESSURE ? sq[k] : 0.0, x, acc,
+                                pacc, 0, 0, 1);
+    }
+  }
+  double4 o;
+  o.x = ex[0] - acc[0];
+  o.y = ex[1] - acc[1];
+  o.z = ex[2] - acc[2];
+  o.w = PRESSURE ? pe - 2.0 * A.mu * pacc : 0.0;
+  reinterpret_cast<double4*>(G.res)[j] = o;
+}
+
+// u[t] += sum over t's pairs (ascending sphere) of du; p[t] likewise.
+template <bool PRESSURE>
+__global__ void k_noff_sum(const NearOffArgs A, const NearGrp G) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= A.M) return;
+  const int j0 = G.off[t], j1 = G.off[t + 1];
+  if (j0 == j1) return;
+  const double4* r4 = reinterpret_cast<const double4*>(G.res);
+  double du0 = 0.0, du1 = 0.0, du2 = 0.0, dp = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double4 o = r4[j];
+    du0 += o.x;
+    du1 += o.y;
+    du2 += o.z;
+    dp += o.w;
+  }
+  A.u[3 * t] += du0;
+  A.u[3 * t + 1] += du1;
+  A.u[3 * t + 2] += du2;
+  if (PRESSURE && A.pres) A.pres[t] += dp;
+}
+
 }  // namespace bie

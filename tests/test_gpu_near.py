@@ -136,14 +136,21 @@ def _near_targets(c, a, n, seed, lo=0.1, hi=1.5):
     return np.array(out)
 
 
-@pytest.mark.parametrize("p,ns,eta,use_p", [(5, 4, 1.0, True), (8, 6, 0.5, True), (6, 3, 2.0, False)])
-def test_offsurface_near_matches_oracle(bie, oracle_mod, p, ns, eta, use_p):
+@pytest.mark.parametrize("sched", [0, 1])
+@pytest.mark.parametrize("p,ns,eta,use_p,m", [(5, 4, 1.0, True, 300), (8, 6, 0.5, True, 300),
+                                              (6, 3, 2.0, False, 300), (4, 2, 1.0, True, 700)])
+def test_offsurface_near_matches_oracle(bie, oracle_mod, p, ns, eta, use_p, m, sched):
+    """Both schedules of the off-surface correction (bie_set_near_off_schedule):
+    0 pairs grouped by sphere -- m = 700 targets around 2 spheres puts > 128
+    pairs (one CTA chunk) on a sphere, so chunks split ragged -- and 1 one
+    thread per Morton-sorted target."""
     c, a, f, q, mu = _random_case(900 + p, ns, p, True, 1.4)
-    tg = _near_targets(c, a, 300, p)
+    tg = _near_targets(c, a, m, p)
     tg = np.concatenate([tg, c[:2] + np.array([[0.1, -0.2, 0.15]])])  # two interior targets
     uref, pref = oracle_mod.offsurface_near(c, a, p, mu, f, q, eta, tg)
     ctx = bie.bie_create(c, a, p, mu)
     bie.bie_set_near(ctx, eta)
+    bie.bie_set_near_off_schedule(ctx, sched)
     u = torch.empty((len(tg), 3), dtype=torch.float64, device="cuda")
     pr = torch.empty(len(tg), dtype=torch.float64, device="cuda") if use_p else None
     bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), _dev(tg), u, pr)
@@ -172,6 +179,55 @@ def test_offsurface_near_config5_subset(bie, oracle_mod):
                                             d["targets"][tsub])
     _assert_parity(u.cpu().numpy()[tsub], uref, "cfg5 near u")
     _assert_parity(pr.cpu().numpy()[tsub], pref, "cfg5 near p")
+
+
+def test_offsurface_near_schedules_agree_config5(bie, oracle_mod):
+    """cfg 5, all 1e6 targets, eta = 1: the grouped schedule (0) against the
+    per-target one (1) element by element (same per-pair arithmetic and the
+    same ascending-sphere sum order up to list-overflow flushes), u and p."""
+    from tests.test_gpu_parity import _cfg_inputs
+    d, f, q = _cfg_inputs(oracle_mod, 5)
+    ctx = bie.bie_create(d["centres"], d["radii"], d["p"], d["mu"])
+    bie.bie_set_near(ctx, 1.0)
+    tg = _dev(d["targets"])
+    M = tg.shape[0]
+    out = []
+    for sched in (0, 1):
+        bie.bie_set_near_off_schedule(ctx, sched)
+        u = torch.empty((M, 3), dtype=torch.float64, device="cuda")
+        pr = torch.empty(M, dtype=torch.float64, device="cuda")
+        bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), tg, u, pr)
+        torch.cuda.synchronize()
+        out.append((u.cpu().numpy(), pr.cpu().numpy()))
+    with pytest.raises(bie.BieError):
+        bie.bie_set_near_off_schedule(ctx, 2)
+    ctx.close()
+    (u0, p0), (u1, p1) = out
+    assert np.abs(u0 - u1).max() <= 1e-13 * np.abs(u1).max()
+    assert np.abs(p0 - p1).max() <= 1e-13 * np.abs(p1).max()
+
+
+def test_offsurface_near_no_pairs_and_high_order(bie, oracle_mod):
+    """Grouped schedule edge cases: targets with no near sphere (pair count 0:
+    the early return) and p = 32, where a sphere's records exceed the 100 KB
+    staging budget (k_noff_grp<.., STAGE = false>)."""
+    c = np.array([[0.0, 0.0, 0.0], [3.0, 0.2, -0.1]])
+    a = np.array([1.0, 0.8])
+    for p, tg in ((6, np.array([[20.0, 0.0, 0.0], [0.0, 30.0, 1.0]])),
+                  (32, _near_targets(c, a, 40, 32))):
+        N = 2 * (p + 1) * (2 * p + 2)
+        rng = np.random.default_rng(p)
+        f, q = rng.standard_normal((N, 3)), rng.standard_normal((N, 3))
+        uref, pref = oracle_mod.offsurface_near(c, a, p, 1.0, f, q, 1.0, tg)
+        ctx = bie.bie_create(c, a, p, 1.0)
+        bie.bie_set_near(ctx, 1.0)
+        u = torch.empty((len(tg), 3), dtype=torch.float64, device="cuda")
+        pr = torch.empty(len(tg), dtype=torch.float64, device="cuda")
+        bie.bie_eval_offsurface(ctx, _dev(f), _dev(q), _dev(tg), u, pr)
+        torch.cuda.synchronize()
+        ctx.close()
+        _assert_parity(u.cpu().numpy(), uref, f"offsurface near p={p} u")
+        _assert_parity(pr.cpu().numpy(), pref, f"offsurface near p={p} p")
 
 
 @pytest.mark.parametrize("p", [24, 30, 32])

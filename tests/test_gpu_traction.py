@@ -158,10 +158,11 @@ def test_K_near_two_spheres_vs_converged_quadrature(bie, oracle_mod, direction):
 
 
 # --------------------------------------- off-surface traction (bie_eval_traction)
-def gpu_traction(bie, c, a, p, mu, sigma, tg, tn, eta=0.0, chunks=0):
+def gpu_traction(bie, c, a, p, mu, sigma, tg, tn, eta=0.0, chunks=0, sched=0):
     ctx = bie.bie_create(c, a, p, mu)
     if eta > 0:
         bie.bie_set_near(ctx, eta)
+        bie.bie_set_near_off_schedule(ctx, sched)
     if chunks:
         bie.bie_set_source_chunks(ctx, chunks)
     t = torch.full((len(tg), 3), np.nan, dtype=torch.float64, device="cuda")
@@ -183,13 +184,15 @@ def _targets_around(seed, c, a, m):
     return tg, nv / np.linalg.norm(nv, axis=1)[:, None]
 
 
-@pytest.mark.parametrize("p,ns,eta,chunks", [(4, 5, 0.0, 0), (6, 7, 1.0, 0), (8, 4, 2.0, 3), (12, 3, 1.0, 0)])
-def test_traction_offsurface_matches_oracle(bie, oracle_mod, p, ns, eta, chunks):
+@pytest.mark.parametrize("p,ns,eta,chunks,sched", [(4, 5, 0.0, 0, 0), (6, 7, 1.0, 0, 0), (8, 4, 2.0, 3, 0),
+                                                    (12, 3, 1.0, 0, 0), (6, 7, 1.0, 0, 1), (12, 3, 1.0, 0, 1)])
+def test_traction_offsurface_matches_oracle(bie, oracle_mod, p, ns, eta, chunks, sched):
+    """sched: bie_set_near_off_schedule (0 grouped by sphere, 1 per target)."""
     c, a, f, _, mu = _random_case(1300 + p, ns, p, True, 1.1)
     tg, nv = _targets_around(p, c, a, 700)
-    got = gpu_traction(bie, c, a, p, mu, f, tg, nv, eta, chunks)
+    got = gpu_traction(bie, c, a, p, mu, f, tg, nv, eta, chunks, sched)
     ref = oracle_mod.traction_offsurface(c, a, p, f, tg, nv, eta)
-    _assert_parity(got, ref, f"traction p={p} eta={eta}")
+    _assert_parity(got, ref, f"traction p={p} eta={eta} sched={sched}")
 
 
 def test_traction_offsurface_closed_forms_on_gpu(bie, oracle_mod):
