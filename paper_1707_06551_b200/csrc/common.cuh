@@ -82,6 +82,24 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 
+// Bulk copy shared -> global through the TMA unit (SASS UBLKCP), tracked as a
+// bulk group of the issuing thread.  The shared-memory writes it reads must be
+// fenced into the async proxy (fence_proxy_async_smem by every writer, then a
+// barrier) first; the issuing thread waits with bulk_wait_read0 before the
+// shared memory may be reused or the CTA exits.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // Bulk prefetch of [src, src + bytes) into L2 (one instruction for a whole
 // contiguous range; src 16-byte aligned, bytes % 16 == 0).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {

@@ -70,6 +70,54 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   const int t = A.tgt[blockIdx.x];
   for (int e = tid; e < 3 * nlm; e += nt) rt[e] = A.tab[L.rA + e];
   for (int e = tid; e < 3 * nsn; e += nt) du[e] = 0.0;
+  if (PART == 2 && STAGE) {
+    // Exterior part alone: only the neighbours' coefficients are read, so the
+    // record region holds a batch of them -- two barriers per batch of B
+    // neighbours instead of per neighbour (ncu r30: k_near<1,1,2> stalled on
+    // barriers, 46 % FP64 pipe).  Same per-node accumulation order.
+    const int B = (12 * nsn + 10 * nlm) / (10 * nlm);
+    const int q0 = A.nb_off[t], q1 = A.nb_off[t + 1];
+    for (int qb = q0; qb < q1; qb += B) {
+      const int nb = min(B, q1 - qb);
+      __syncthreads();  // previous batch no longer in use (and du / rt ready)
+      for (int j = 0; j < nb; ++j) {
+        const double2* c2 = reinterpret_cast<const double2*>(A.coef + (int64_t)A.nb_idx[qb + j] * nlm * 10);
+        double2* d2 = reinterpret_cast<double2*>(srec + j * 10 * nlm);
+        for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
+      }
+      __syncthreads();
+      for (int kk = tid; kk < nsn; kk += nt) {
+        const int64_t i = (int64_t)t * nsn + kk;
+        const double* ri = A.rec + i * kRec;
+        const double xt[3] = {ri[0], ri[1], ri[2]};
+        double nx[3] = {0.0, 0.0, 0.0};
+        if constexpr (K) {
+          nx[0] = ri[3];
+          nx[1] = ri[4];
+          nx[2] = ri[5];
+        }
+        double d0 = du[3 * kk], d1 = du[3 * kk + 1], d2 = du[3 * kk + 2];
+        for (int j = 0; j < nb; ++j) {
+          const int s = A.nb_idx[qb + j];
+          const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+          const double a = A.radii[s];
+          const double* cfj = srec + j * 10 * nlm;
+          double ex[3];
+          if constexpr (K) exterior_traction(p, cfj, rt, rt + nlm, cs, a, xt, nx, ex);
+          else exterior_field<false>(p, cfj, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
+          d0 += ex[0] - 0.0;
+          d1 += ex[1] - 0.0;
+          d2 += ex[2] - 0.0;
+        }
+        du[3 * kk] = d0;
+        du[3 * kk + 1] = d1;
+        du[3 * kk + 2] = d2;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
+    return;
+  }
   for (int qn = A.nb_off[t]; qn < A.nb_off[t + 1]; ++qn) {
     const int s = A.nb_idx[qn];
     const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
@@ -78,15 +126,17 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
     const double* rec_s = A.rec + (int64_t)s * nsn * kRec;
     if (STAGE) {
       __syncthreads();  // previous neighbour's staged data no longer in use
-      const double2* g2 = reinterpret_cast<const double2*>(rec_s);
-      double2* s2 = reinterpret_cast<double2*>(srec);
-      for (int e = tid; e < 6 * nsn; e += nt) s2[e] = g2[e];
+      if (PART != 2) {  // (the exterior part alone needs only the coefficients)
+        const double2* g2 = reinterpret_cast<const double2*>(rec_s);
+        double2* s2 = reinterpret_cast<double2*>(srec);
+        for (int e = tid; e < 6 * nsn; e += nt) s2[e] = g2[e];
+        rec_s = srec;
+      }
       const double2* c2 = reinterpret_cast<const double2*>(cf);
       double2* d2 = reinterpret_cast<double2*>(scf);
       for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
       __syncthreads();
       cf = scf;
-      rec_s = srec;
     } else if (qn == A.nb_off[t]) {
       __syncthreads();
     }

@@ -43,8 +43,20 @@ struct SelfArgs {
   int precond;      // 1: u = P^{-1} q with P = 1/2 I + S_self + D_self (f ignored):
                     //    eigenvalue 1/(1/2 + lamS a/mu + lamD) on every VSH mode of
                     //    degree <= p and 2 on the rest (NEXT-2 preconditioner)
+  int out_stage = 0;  // k_self_t: records (and u) staged in shared memory and written
+                      // by TMA bulk stores (launch with self_smem_bytes(p, SPC, true))
 };
 
+__host__ __device__ inline int64_t self_smem_doubles(int p);
+// Dynamic shared memory of k_self_t for SPC spheres per CTA; out_stage adds
+// the SPC x 12 nsn-double record staging area.  (Staging the Legendre tables
+// P, dP, mPs as well -- one more bulk copy -- measured slower at p = 6, 8, 12:
+// profiles/r02_self_tune.jsonl, r34.)
+inline size_t self_smem_bytes(int p, int spc, bool out_stage) {
+  const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
+  return (size_t)(spc * (6 * nsn + 12 * P1 * P1) + 2 * nphi + 2 + (out_stage ? spc * 12 * nsn : 0)) *
+         sizeof(double);
+}
 __host__ __device__ inline int64_t self_smem_doubles(int p) {
   const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
   const int64_t C = 6LL * nsn;       // spherical components; reused as ALPHA, then U
@@ -69,6 +81,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   const int SZ = 6 * nsn + 12 * P1 * P1;  // per sphere: C [2][3][nsn] + F [2][3][P1][P1][2]
   double2* tw = reinterpret_cast<double2*>(sm + SPC * SZ);  // (cos, sin)(2 pi q/nphi), shared
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SPC * SZ + 2 * nphi);
+  // out_stage: per-sphere packed records [nsn][12], written by one TMA bulk store
+  auto Rp = [&](int sp) { return sm + SPC * SZ + 2 * nphi + 2 + sp * 12 * nsn; };
   // per-sphere views: C; F (PSI aliases F, dead after phase C); U aliases C
   auto Cp = [&](int sp) { return sm + sp * SZ; };
   auto Fp_ = [&](int sp) { return sm + sp * SZ + 6 * nsn; };
@@ -105,6 +119,18 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     const double ct = tab[L.t + j], st = tab[L.st + j];
     const double cp = tw[k].x, sp_ = tw[k].y;
     const double n0 = st * cp, n1 = st * sp_, n2 = ct;
+    if (A.out_stage) {  // packed source record (row a2) into the staging area
+      const double a = ra[sp];
+      const double w = a * a * tab[L.wu + j];
+      const double ws = w * cS, wd = w * cD;
+      double2* r2 = reinterpret_cast<double2*>(Rp(sp) + kk * kRec);
+      r2[0] = make_double2(rcx[sp] + a * n0, rcy[sp] + a * n1);
+      r2[1] = make_double2(rcz[sp] + a * n2, n0);
+      r2[2] = make_double2(n1, n2);
+      r2[3] = make_double2(ws * f0, ws * f1);
+      r2[4] = make_double2(ws * f2, wd * q0);
+      r2[5] = make_double2(wd * q1, wd * q2);
+    }
     // e_r = n, e_theta = (ct cp, ct sp, -st), e_phi = (-sp, cp, 0)
     g[0] = aS * (f0 * n0 + f1 * n1 + f2 * n2);
     g[1] = aS * (f0 * ct * cp + f1 * ct * sp_ - f2 * st);
@@ -151,11 +177,12 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   }
   mbar_wait(bar, 0);
   // -------------------------------------------------------------- A1 records
-  // Packed source records (row a2), written as consecutive 16-byte chunks so
-  // that a warp's stores cover contiguous 512 bytes.
+  // Without out_stage (shared memory too small): packed source records (row
+  // a2) written as consecutive 16-byte chunks so that a warp's stores cover
+  // contiguous 512 bytes.
 #pragma unroll
   for (int sp = 0; sp < SPC; ++sp) {
-    if (!valid[sp]) continue;
+    if (!valid[sp] || A.out_stage) continue;
     const double* Fs = Fp_(sp);
     const double a = ra[sp];
     double2* out = reinterpret_cast<double2*>(A.rec + sidx[sp] * nsn * kRec);
@@ -186,10 +213,11 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
 #pragma unroll
     for (int sp = 0; sp < SPC; ++sp) {
       if (!valid[sp]) continue;
-      if (spec) {
+      if (spec || A.out_stage) {
         double g1[6], g2[6];
         node(sp, j, k, g1);
         if (pair) node(sp, j, nphi - k, g2);
+        if (!spec) continue;
         double* row = Cp(sp) + j * nphi;
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
@@ -209,11 +237,21 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
       if (valid[sp] && A.u)
         for (int e = tid; e < 3 * nsn; e += nt) A.u[sidx[sp] * 3 * nsn + e] = 0.0;
   };
+  // out_stage: the staged records leave through one TMA bulk store per sphere
+  // (no LSU wavefronts; the issuing thread waits for its reads before exit)
+  if (A.out_stage) fence_proxy_async_smem();
+  __syncthreads();
+  if (A.out_stage && tid == 0) {
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp)
+      if (valid[sp]) bulk_s2g(A.rec + sidx[sp] * nsn * kRec, Rp(sp), (uint32_t)(nsn * kRec * sizeof(double)));
+    bulk_commit();
+  }
   if (!spec) {
     zero_u();
+    if (A.out_stage && tid == 0) bulk_wait_read0();
     return;
   }
-  __syncthreads();
   // ---------------------------------------------------------------- B
   // F[dc][j][m] = sum_k g[k] e^{-i m phi_k}
   //   = g0 + (-1)^m g_{p+1} + sum_{k=1}^{p} S_k cos(m phi_k) - i sum_k D_k sin(m phi_k)
@@ -298,6 +336,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   }
   if (!A.self) {
     zero_u();
+    if (A.out_stage && tid == 0) bulk_wait_read0();
     return;
   }
   __syncthreads();
@@ -408,7 +447,10 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // Inverse DFT for the node pair (k, nphi-k) of a latitude:
   //   u(k) = U0 + 2(c - s), u(nphi-k) = U0 + 2(c + s),
   //   c = sum_m Re U_m cos(m phi_k), s = sum_m Im U_m sin(m phi_k),
-  // then spherical -> Cartesian components and the store of u_self.
+  // then spherical -> Cartesian components and the store of u_self (out_stage
+  // with a 16-byte-aligned u: into F, dead after phase D, then one TMA bulk
+  // store per sphere).
+  const bool ustage = A.out_stage && !(reinterpret_cast<uintptr_t>(A.u) & 15);
   for (int it = tid; it < P1 * (P1 + 1); it += nt) {
     const int j = it / (P1 + 1), k = it % (P1 + 1);
     double c[SPC][3], sn_[SPC][3];
@@ -457,26 +499,42 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
           w1 = fma(2.0, A.q[3 * i + 1], w1);
           w2 = fma(2.0, A.q[3 * i + 2], w2);
         }
-        A.u[3 * i + 0] = w0;
-        A.u[3 * i + 1] = w1;
-        A.u[3 * i + 2] = w2;
+        double* uo = ustage ? Fp_(sp) + 3 * (j * nphi + kk) : A.u + 3 * i;
+        uo[0] = w0;
+        uo[1] = w1;
+        uo[2] = w2;
       }
     }
   }
+  if (ustage) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int sp = 0; sp < SPC; ++sp)
+        if (valid[sp]) bulk_s2g(A.u + sidx[sp] * 3 * nsn, Fp_(sp), (uint32_t)(3 * nsn * sizeof(double)));
+      bulk_commit();
+    }
+  }
+  if (A.out_stage && tid == 0) bulk_wait_read0();
 }
 
 // Launch configurations chosen by tools/self_tune.cu (profiles/r01_self_tune.txt,
-// re-swept after the TMA staging in profiles/r02_self_tune.jsonl): p <= 6 many
-// 64-thread CTAs (64 registers, 16 per SM), p = 8 and 12 128 threads.
-// The orders of the BASELINE configurations (4, 6, 8, 12) get compile-time-p
-// instantiations; every other p runs the generic kernel.
-inline void launch_self(const SelfArgs& A, cudaStream_t s) {
-  const size_t smem = self_smem_doubles(A.p) * sizeof(double);
+// re-swept with the TMA staging in profiles/r02_self_tune.jsonl): p <= 8 many
+// 64-thread CTAs, p = 12 128 threads.  The orders of the BASELINE
+// configurations (4, 6, 8, 12) get compile-time-p instantiations; every other
+// p runs the generic kernel.  Outputs are staged (out_stage) whenever the
+// staging area fits the 227 KB opt-in (p <= 22 for one sphere per CTA).
+inline bool self_out_stage(int p, int spc) { return self_smem_bytes(p, spc, true) <= 227 * 1024; }
+inline void launch_self(const SelfArgs& A0, cudaStream_t s) {
+  SelfArgs A = A0;
+  A.out_stage = self_out_stage(A.p, 1) ? 1 : 0;
+  const size_t smem = self_smem_bytes(A.p, 1, A.out_stage);
   const unsigned g = (unsigned)A.ns;
   switch (A.p) {
-    case 4: k_self_t<64, 16, 4><<<g, 64, smem, s>>>(A); break;
-    case 6: k_self_t<64, 16, 6><<<g, 64, smem, s>>>(A); break;
-    case 8: k_self_t<128, 6, 8><<<g, 128, smem, s>>>(A); break;
+    case 4: k_self_t<64, 12, 4><<<g, 64, smem, s>>>(A); break;
+    case 6: k_self_t<64, 12, 6><<<g, 64, smem, s>>>(A); break;
+    case 8: k_self_t<64, 12, 8><<<g, 64, smem, s>>>(A); break;
     case 12: k_self_t<128, 5, 12><<<g, 128, smem, s>>>(A); break;
     default:
       if (A.p <= 8) k_self_t<64, 12><<<g, 64, smem, s>>>(A);
@@ -486,12 +544,11 @@ inline void launch_self(const SelfArgs& A, cudaStream_t s) {
 // Two spheres per CTA (SPC = 2): independent work per thread for the scheduler
 // to interleave; same phases and barriers (measured against SPC = 1 in
 // profiles/r02_self_bench.jsonl).
-inline size_t self2_smem_bytes(int p) {
-  const int P1 = p + 1, nphi = 2 * p + 2, nsn = P1 * nphi;
-  return (size_t)(2 * (6 * nsn + 12 * P1 * P1) + 2 * nphi + 2) * sizeof(double);
-}
-inline void launch_self2(const SelfArgs& A, cudaStream_t s) {
-  const size_t smem = self2_smem_bytes(A.p);
+inline size_t self2_smem_bytes(int p) { return self_smem_bytes(p, 2, false); }
+inline void launch_self2(const SelfArgs& A0, cudaStream_t s) {
+  SelfArgs A = A0;
+  A.out_stage = self_out_stage(A.p, 2) ? 1 : 0;
+  const size_t smem = self_smem_bytes(A.p, 2, A.out_stage);
   const unsigned g = (unsigned)((A.ns + 1) / 2);
   switch (A.p) {
     case 4: k_self_t<64, 8, 4, 2><<<g, 64, smem, s>>>(A); break;
@@ -505,7 +562,7 @@ inline void launch_self2(const SelfArgs& A, cudaStream_t s) {
 }
 
 inline void set_self_smem(int p) {
-  const int smem2 = (int)self2_smem_bytes(p);
+  const int smem2 = (int)self_smem_bytes(p, 2, self_out_stage(p, 2));
   if (smem2 <= 227 * 1024) {
     cudaFuncSetAttribute(k_self_t<64, 8, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     cudaFuncSetAttribute(k_self_t<64, 8, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
@@ -514,12 +571,12 @@ inline void set_self_smem(int p) {
     cudaFuncSetAttribute(k_self_t<64, 8, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     cudaFuncSetAttribute(k_self_t<128, 3, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   }
-  const int smem = (int)(self_smem_doubles(p) * sizeof(double));
+  const int smem = (int)self_smem_bytes(p, 1, self_out_stage(p, 1));
   cudaFuncSetAttribute(k_self_t<64, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_self_t<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<64, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<64, 16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_self_t<128, 6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 12, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_self_t<64, 12, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_self_t<128, 5, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 

@@ -120,6 +120,34 @@ def test_self_term_kernel_variants(bie, oracle_mod, p, variant):
     ctx.close()
 
 
+@pytest.mark.parametrize("p", [6, 12, 24])
+def test_self_term_unaligned_views(bie, oracle_mod, p):
+    """f, q, u passed as views offset by one double (8-byte, not 16-byte,
+    aligned): k_self_t's TMA bulk loads of f, q and its bulk store of u need
+    16-byte alignment, so it falls back to cooperative loads and direct
+    stores.  Same values as the aligned call, and parity with the oracle."""
+    c, a, f, q, mu = _random_case(760 + p, 3, p, True, 1.1)
+    ctx = bie.bie_create(c, a, p, mu)
+    N = bie.bie_num_nodes(ctx)
+
+    def view(x):
+        buf = torch.full((3 * N + 1,), np.nan, dtype=torch.float64, device="cuda")
+        v = buf[1:].view(N, 3)
+        if x is not None:
+            v.copy_(torch.from_numpy(x))
+        assert v.data_ptr() % 16 == 8
+        return v
+    fu, qu, uu = view(f), view(q), view(None)
+    bie.bie_apply_parts(ctx, fu, qu, uu, bie.BIE_PART_SELF)
+    ua = torch.full((N, 3), np.nan, dtype=torch.float64, device="cuda")
+    bie.bie_apply_parts(ctx, _dev(f), _dev(q), ua, bie.BIE_PART_SELF)
+    torch.cuda.synchronize()
+    ctx.close()
+    got = uu.cpu().numpy()
+    assert np.array_equal(got, ua.cpu().numpy())
+    _assert_parity(got, oracle_mod.self_term(c, a, p, mu, f, q), f"self unaligned p={p}")
+
+
 # ------------------------------------------------------------- a3 far field
 @pytest.mark.parametrize("p,ns,chunks", [(4, 2, 0), (4, 7, 3), (6, 9, 0), (8, 5, 1), (5, 3, 2)])
 def test_far_field_only(bie, oracle_mod, p, ns, chunks):

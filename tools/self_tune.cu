@@ -13,7 +13,7 @@ static char* g_flush = nullptr;  // 256 MB written before every timed launch (L2
 
 template <int TPB, int MINB, int PT = 0, int SPC = 1>
 void run(const char* name, SelfArgs A, int64_t N) {
-  const size_t smem = SPC == 1 ? self_smem_doubles(A.p) * sizeof(double) : self2_smem_bytes(A.p);
+  const size_t smem = self_smem_bytes(A.p, SPC, A.out_stage != 0);
   cudaFuncSetAttribute(k_self_t<TPB, MINB, PT, SPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_self_t<TPB, MINB, PT, SPC>, TPB, smem);
@@ -33,9 +33,18 @@ void run(const char* name, SelfArgs A, int64_t N) {
     cudaEventElapsedTime(&ms, e0, e1);
     if (r > 1 && ms < best) best = ms;
   }
-  printf("{\"p\": %d, \"variant\": \"%s\", \"regs\": %d, \"spill\": %d, \"occ\": %d, \"us\": %.2f, \"GBps\": %.1f, \"err\": \"%s\"}\n",
-         A.p, name, fa.numRegs, (int)fa.localSizeBytes, occ, best * 1e3, 168.0 * N / (best * 1e-3) / 1e9,
+  printf("{\"p\": %d, \"out_stage\": %d, \"variant\": \"%s\", \"regs\": %d, \"spill\": %d, \"occ\": %d, \"us\": %.2f, \"GBps\": %.1f, \"err\": \"%s\"}\n",
+         A.p, A.out_stage, name, fa.numRegs, (int)fa.localSizeBytes, occ, best * 1e3, 168.0 * N / (best * 1e-3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
+}
+
+// both output paths: direct global stores, and staged + TMA bulk stores
+template <int TPB, int MINB, int PT = 0, int SPC = 1>
+void both(const char* name, SelfArgs A, int64_t N) {
+  A.out_stage = 0;
+  run<TPB, MINB, PT, SPC>(name, A, N);
+  A.out_stage = 1;
+  run<TPB, MINB, PT, SPC>(name, A, N);
 }
 
 int main() {
@@ -68,32 +77,23 @@ int main() {
     SelfArgs A{};
     A.p = p; A.ns = ns; A.mu = 1.0; A.tab = tab; A.centres = cen; A.radii = rad;
     A.f = f; A.q = q; A.u = u; A.rec = rec; A.self = 1; A.alpha = nullptr; A.precond = 0;
-    run<64, 12>("T64 minB12 generic", A, N);
-    run<128, 4>("T128 minB4 generic", A, N);
     if (p == 6) {
-      run<64, 12, 6>("T64 minB12 PT=6", A, N);
-      run<64, 16, 6>("T64 minB16 PT=6", A, N);
-      run<64, 8, 6, 2>("T64 minB8 PT=6 SPC2", A, N);
-      run<64, 10, 6, 2>("T64 minB10 PT=6 SPC2", A, N);
-      run<128, 6, 6>("T128 minB6 PT=6", A, N);
-      run<128, 8, 6>("T128 minB8 PT=6", A, N);
-      run<32, 16, 6>("T32 minB16 PT=6", A, N);
-      run<32, 24, 6>("T32 minB24 PT=6", A, N);
-      run<32, 32, 6>("T32 minB32 PT=6", A, N);
+      both<64, 12, 6>("T64 minB12 PT=6", A, N);
+      both<64, 16, 6>("T64 minB16 PT=6", A, N);
+      both<64, 8, 6, 2>("T64 minB8 PT=6 SPC2", A, N);
+      both<128, 6, 6>("T128 minB6 PT=6", A, N);
+      both<32, 24, 6>("T32 minB24 PT=6", A, N);
     } else if (p == 8) {
-      run<64, 12, 8>("T64 minB12 PT=8", A, N);
-      run<64, 16, 8>("T64 minB16 PT=8", A, N);
-      run<64, 8, 8, 2>("T64 minB8 PT=8 SPC2", A, N);
-      run<128, 6, 8>("T128 minB6 PT=8", A, N);
-      run<32, 24, 8>("T32 minB24 PT=8", A, N);
+      both<64, 12, 8>("T64 minB12 PT=8", A, N);
+      both<64, 16, 8>("T64 minB16 PT=8", A, N);
+      both<64, 8, 8, 2>("T64 minB8 PT=8 SPC2", A, N);
+      both<128, 6, 8>("T128 minB6 PT=8", A, N);
+      both<32, 24, 8>("T32 minB24 PT=8", A, N);
     } else {
-      run<128, 4, 12>("T128 minB4 PT=12", A, N);
-      run<128, 5, 12>("T128 minB5 PT=12", A, N);
-      run<128, 6, 12>("T128 minB6 PT=12", A, N);
-      run<128, 3, 12, 2>("T128 minB3 PT=12 SPC2", A, N);
-      run<256, 3, 12>("T256 minB3 PT=12", A, N);
-      run<64, 8, 12>("T64 minB8 PT=12", A, N);
-      run<64, 10, 12>("T64 minB10 PT=12", A, N);
+      both<128, 3, 12>("T128 minB3 PT=12", A, N);
+      both<128, 5, 12>("T128 minB5 PT=12", A, N);
+      both<256, 2, 12>("T256 minB2 PT=12", A, N);
+      both<64, 8, 12>("T64 minB8 PT=12", A, N);
     }
     cudaFree(tab); cudaFree(cen); cudaFree(rad); cudaFree(f); cudaFree(q); cudaFree(u); cudaFree(rec);
   }
