@@ -357,8 +357,16 @@ int bie_set_self_kernel(bie_ctx* ctx, int variant);
 /*
  * Measurement knob: the schedule of the far-field pair-sum kernels.
  * 1 (default): source chunks chosen by a wave-aware planner, one CTA per
- *   (target tile, chunk) dispatched by the hardware, chunk partials in HBM, a
- *   fixed-order reduction kernel.
+ *   (target tile, chunk).  With >= 16 such units per resident CTA slot the
+ *   chunks of a tile are summed inside the kernel (as 5), below that through
+ *   HBM partials and a fixed-order reduction kernel (as 6).
+ * 5: chained in-kernel reduction -- CTAs take (chunk, tile) from a ticket
+ *   counter in chunk-major order; chunk c of a tile waits for chunk c - 1's
+ *   release flag, adds its partial to the tile's running sum and releases c + 1;
+ *   the last chunk writes u.  Same fixed summation order as 6 (bit-identical
+ *   results), no chunk partials in HBM, no reduction launch.  A wait longer
+ *   than 60 s traps (the launch then fails with BIE_ERR_CUDA) instead of hanging.
+ * 6: chunk partials in HBM + the fixed-order reduction kernel.
  * 0: stream-K -- one persistent CTA per resident slot, each given an equal
  *   contiguous range of (target tile, source tile) units; a target tile whose
  *   units span several CTAs is finished by a fixed-order fix-up kernel from at
@@ -368,9 +376,9 @@ int bie_set_self_kernel(bie_ctx* ctx, int variant);
  *   the 8 / 4 / 16 source chunks of a target tile run as ONE thread-block
  *   cluster (16: apply only, non-portable size) and are summed on chip through
  *   distributed shared memory in fixed rank order; smaller launches use 1.
- * bie_set_source_chunks > 0 forces schedule 1.  All schedules are
- * deterministic; they differ only in fp64 summation grouping.  BIE_ERR_ARG
- * outside 0..4.
+ * bie_set_source_chunks > 0 forces the chunked schedules (1, 5 or 6).  All
+ * schedules are deterministic; they differ only in fp64 summation grouping
+ * (1, 5 and 6 not at all).  BIE_ERR_ARG outside 0..6.
  */
 int bie_set_far_reduction(bie_ctx* ctx, int mode);
 

@@ -88,7 +88,12 @@ struct bie_ctx {
   int self_variant = -1;    // -1 auto (fastest measured per order), 0 k_sht DMMA, 1 k_sht DFMA,
                             // 2 round-1 k_self_t
   int chunks_override = 0;
-  int far_red = 1;  // bie_set_far_reduction: 0 stream-K, 1 chunks + k_reduce (default), 2/3/4 clusters
+  int far_red = 1;  // bie_set_far_reduction: 0 stream-K, 1 chunks (default; chained or k_reduce by
+                    // size), 2/3/4 clusters, 5 chunks always chained, 6 chunks always + k_reduce
+  double* d_cacc = nullptr;  // chained reduction: running sums [M][4]
+  size_t cacc_cap = 0;       // doubles
+  int* d_chain = nullptr;    // chained reduction: per-tile flags + ticket counter
+  size_t chain_cap = 0;      // ints
   int occ_sk[4] = {1, 1, 1, 1};
   int occ_apply_nx = 1, occ_K_nx = 1;  // resident CTAs per SM of the near-exclusion kernels  // resident CTAs per SM of the stream-K kernels (apply, off, K, offK)
   // near-singular correction (NEXT-1)
@@ -347,6 +352,51 @@ static int ensure_part(bie_ctx* c, size_t doubles) {
   }
   c->part_cap = doubles;
   return BIE_OK;
+}
+
+// Chained chunk reduction (bie_set_far_reduction 5): the running-sum buffer
+// ([M][3] + [M] pressure) and the n_tt flags + ticket counter, zeroed on the
+// stream before the launch (a launch that died mid-way cannot leave stale flags).
+static int setup_chain(bie_ctx* c, NbodyArgs& A, int64_t M, cudaStream_t s) {
+  const size_t nd = (size_t)4 * M, ni = (size_t)A.n_tt + 1;
+  if (nd > c->cacc_cap) {
+    cudaFree(c->d_cacc);
+    c->d_cacc = nullptr;
+    c->cacc_cap = 0;
+    if (cudaMalloc(&c->d_cacc, nd * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, BIE_ERR_ALLOC, "cannot allocate the chained-reduction sums%s");
+    }
+    c->cacc_cap = nd;
+  }
+  if (ni > c->chain_cap) {
+    cudaFree(c->d_chain);
+    c->d_chain = nullptr;
+    c->chain_cap = 0;
+    if (cudaMalloc(&c->d_chain, ni * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, BIE_ERR_ALLOC, "cannot allocate the chained-reduction flags%s");
+    }
+    c->chain_cap = ni;
+  }
+  cudaError_t e = cudaMemsetAsync(c->d_chain, 0, ni * sizeof(int), s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "chained reduction flags");
+  A.chain = c->d_chain;
+  A.cacc = c->d_cacc;
+  return BIE_OK;
+}
+
+// Chained in-kernel reduction (5) or HBM partials + k_reduce (6) for a chunked
+// launch; the default (1) chains when the launch has >= 16 units per resident
+// CTA slot -- then chunk c - 1 of a tile finished long before chunk c does --
+// and uses k_reduce below that, where the chunks of a tile run side by side
+// and a chained CTA would idle waiting for its predecessor (cfg 2: 0.33 vs
+// 0.24 ms, profiles/r02_far_reduction.jsonl).
+static bool use_chain(const bie_ctx* c, const ChunkPlan& P, int occ) {
+  if (c->far_red == 5) return true;
+  if (c->far_red != 1) return false;
+  const int64_t slots = (int64_t)c->sm_count * std::max(occ, 1);
+  return (int64_t)P.n_tt * P.n_chunks >= 16 * slots;
 }
 
 static int launch_check(bie_ctx* c, const char* what) {
@@ -762,7 +812,7 @@ static cudaError_t launch_cluster(Kern kern, int n_tt, size_t smem, cudaStream_t
 // launch leaves >= 16 units per resident slot and no chunk count is forced.
 // (Measured on cfg 5, profiles/r02_far_reduction.jsonl: see DESIGN.md §5.)
 static int cluster_size(const bie_ctx* c, const ChunkPlan& P, int occ, int64_t n_src_tiles, bool apply) {
-  if (c->chunks_override > 0 || c->far_red < 2) return 0;
+  if (c->chunks_override > 0 || c->far_red < 2 || c->far_red > 4) return 0;
   const int cl = !apply ? kCL : (c->far_red == 3 ? 4 : (c->far_red == 4 ? 16 : kCL));
   const int64_t slots = (int64_t)c->sm_count * std::max(occ, 1);
   return (P.n_chunks > 1 && n_src_tiles >= 2 * cl && (int64_t)P.n_tt * cl >= 16 * slots) ? cl : 0;
@@ -804,6 +854,8 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode, bool nx) {
   A.rec = c->d_rec;
   A.qn3 = nullptr;
   A.tx = nullptr;
+  A.txa = c->d_x;  // compact target positions / normals (not the 96-byte records)
+  A.tna = c->d_n;
   A.N = c->N;
   A.M = c->N;
   A.nsn = c->nsn;
@@ -827,14 +879,22 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode, bool nx) {
       prof_end(c, s, &ev);
       return launch_check(c, "k_nbody (near exclusion)");
     }
-    if ((rc = ensure_part(c, (size_t)P.n_chunks * 3 * c->N))) return rc;
-    A.uinit = nullptr;
-    A.uout = c->d_part;
+    const bool chain = use_chain(c, P, mode ? c->occ_K_nx : c->occ_apply_nx);
+    if (chain) {
+      if ((rc = setup_chain(c, A, c->N, s))) return rc;
+      A.uinit = u;
+      A.uout = u;
+    } else {
+      if ((rc = ensure_part(c, (size_t)P.n_chunks * 3 * c->N))) return rc;
+      A.uinit = nullptr;
+      A.uout = c->d_part;
+    }
     prof_begin(c, kind, s, &ev);
     if (mode) NBODY_K_NX<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, sm_nx, s>>>(A);
     else NBODY_APPLY_NX<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, sm_nx, s>>>(A);
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_nbody (near exclusion)"))) return rc;
+    if (chain) return BIE_OK;
     prof_begin(c, BIE_KIND_REDUCE, s, &ev);
     k_reduce<<<(unsigned)((3 * c->N + 255) / 256), 256, 0, s>>>(c->N, P.n_chunks, c->d_part, u, u, nullptr,
                                                                  nullptr, 0.0);
@@ -872,16 +932,24 @@ static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode, bool nx) {
     prof_end(c, s, &ev);
     return launch_check(c, "k_nbody");
   }
-  rc = ensure_part(c, (size_t)P.n_chunks * 3 * c->N);
-  if (rc) return rc;
-  A.uinit = nullptr;
-  A.uout = c->d_part;
+  const bool chain = use_chain(c, P, mode ? c->occ_K : c->occ_apply);
+  if (chain) {
+    if ((rc = setup_chain(c, A, c->N, s))) return rc;
+    A.uinit = u;
+    A.uout = u;
+  } else {
+    rc = ensure_part(c, (size_t)P.n_chunks * 3 * c->N);
+    if (rc) return rc;
+    A.uinit = nullptr;
+    A.uout = c->d_part;
+  }
   prof_begin(c, kind, s, &ev);
   if (mode) NBODY_K<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
   else NBODY_APPLY<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
   prof_end(c, s, &ev);
   rc = launch_check(c, "k_nbody");
   if (rc) return rc;
+  if (chain) return BIE_OK;
   prof_begin(c, BIE_KIND_REDUCE, s, &ev);
   k_reduce<<<(unsigned)((3 * c->N + 255) / 256), 256, 0, s>>>(c->N, P.n_chunks, c->d_part, u, u,
                                                                nullptr, nullptr, 0.0);
@@ -956,15 +1024,23 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
       if (rc) return rc;
       continue;
     }
-    rc = ensure_part(c, (size_t)P.n_chunks * 4 * Mb);
-    if (rc) return rc;
-    A.uout = c->d_part;
-    A.pout = p ? c->d_part + (size_t)P.n_chunks * 3 * Mb : nullptr;
+    const bool chain = use_chain(c, P, c->occ_off);
+    if (chain) {
+      if ((rc = setup_chain(c, A, Mb, s))) return rc;
+      A.uout = u + 3 * b0;
+      A.pout = p ? p + b0 : nullptr;
+    } else {
+      rc = ensure_part(c, (size_t)P.n_chunks * 4 * Mb);
+      if (rc) return rc;
+      A.uout = c->d_part;
+      A.pout = p ? c->d_part + (size_t)P.n_chunks * 3 * Mb : nullptr;
+    }
     prof_begin(c, BIE_KIND_OFFSURF, s, &ev);
     NBODY_OFF<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
     prof_end(c, s, &ev);
     rc = launch_check(c, "k_nbody_off");
     if (rc) return rc;
+    if (chain) continue;
     prof_begin(c, BIE_KIND_REDUCE, s, &ev);
     k_reduce<<<(unsigned)((3 * Mb + 255) / 256), 256, 0, s>>>(
         Mb, P.n_chunks, c->d_part, nullptr, u + 3 * b0, A.pout, p ? p + b0 : nullptr, 2.0 * c->mu);
@@ -1045,12 +1121,19 @@ static int run_traction(bie_ctx* c, const double* sigma, const double* tg, const
       if ((rc = launch_check(c, "k_nbody_offK"))) return rc;
       continue;
     }
-    if ((rc = ensure_part(c, (size_t)P.n_chunks * 4 * Mb))) return rc;
-    A.uout = c->d_part;
+    const bool chain = use_chain(c, P, c->occ_offK);
+    if (chain) {
+      if ((rc = setup_chain(c, A, Mb, s))) return rc;
+      A.uout = t + 3 * b0;
+    } else {
+      if ((rc = ensure_part(c, (size_t)P.n_chunks * 4 * Mb))) return rc;
+      A.uout = c->d_part;
+    }
     prof_begin(c, BIE_KIND_KFAR, s, &ev);
     NBODY_OFFK<<<(unsigned)((int64_t)P.n_tt * P.n_chunks), kTPB, nb_smem, s>>>(A);
     prof_end(c, s, &ev);
     if ((rc = launch_check(c, "k_nbody_offK"))) return rc;
+    if (chain) continue;
     prof_begin(c, BIE_KIND_REDUCE, s, &ev);
     k_reduce<<<(unsigned)((3 * Mb + 255) / 256), 256, 0, s>>>(Mb, P.n_chunks, c->d_part, nullptr,
                                                                 t + 3 * b0, nullptr, nullptr, 0.0);
@@ -1093,6 +1176,8 @@ void bie_destroy(bie_ctx* c) {
   if (c->d_delta) cudaFree(c->d_delta);
   if (c->d_deltaT) cudaFree(c->d_deltaT);
   if (c->d_psinear) cudaFree(c->d_psinear);
+  cudaFree(c->d_cacc);
+  cudaFree(c->d_chain);
   cudaFree(c->d_cell_start);
   cudaFree(c->d_cell_items);
   cudaFree(c->d_sort);
@@ -1899,7 +1984,7 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
 
 int bie_set_far_reduction(bie_ctx* c, int mode) {
   if (!c) return BIE_ERR_ARG;
-  if (mode < 0 || mode > 4) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..4%s");
+  if (mode < 0 || mode > 6) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..6%s");
   c->far_red = mode;
   return BIE_OK;
 }

@@ -406,7 +406,7 @@ def test_far_schedules_agree(bie, oracle_mod):
     N = F.shape[0]
     tg = _dev(d["targets"][:600000])
     out = {}
-    for mode in (0, 1, 2, 0):
+    for mode in (0, 1, 2, 5, 6, 0):
         bie.bie_set_far_reduction(ctx, mode)
         u = torch.empty((N, 3), dtype=torch.float64, device="cuda")
         bie.bie_apply_SLDL(ctx, F, Q, u)
@@ -421,6 +421,8 @@ def test_far_schedules_agree(bie, oracle_mod):
             assert all(np.array_equal(a, b) for a, b in zip(out[mode], res)), "not deterministic"
         out[mode] = res
     ctx.close()
+    for m in (5, 6):  # the default (1) chains at this size; 5 always, 6 never: same sums
+        assert all(np.array_equal(a + 0.0, b + 0.0) for a, b in zip(out[1], out[m])), ("chained", m)
     for m in (1, 2):
         for a, b, what in zip(out[0], out[m], ("apply", "offsurface u", "offsurface p", "K")):
             rel, mx = _err(a, b)
@@ -453,3 +455,57 @@ def test_stream_k_small_and_ragged(bie, oracle_mod, ns, p):
     ctx.close()
     _assert_parity(u.cpu().numpy(), uref, "sk off u")
     _assert_parity(pr.cpu().numpy(), pref, "sk off p")
+
+
+@pytest.mark.parametrize("ns,p,chunks", [(3, 4, 2), (7, 6, 3), (40, 5, 7), (12, 8, 0), (2, 1, 2)])
+def test_chained_reduction_matches_k_reduce(bie, oracle_mod, ns, p, chunks):
+    """bie_set_far_reduction(5): the chunk partials are summed inside the
+    far-field kernel (ticket order, chunk c waits for c - 1 of its tile) in
+    k_reduce's fixed order, so every far-field output -- apply (with and without
+    near exclusion), K apply, off-surface u / p, off-surface traction -- equals
+    schedule 6's (HBM partials + k_reduce) bit for bit, and both match the oracle."""
+    c, a, f, q, mu = _random_case(1400 + ns + p, ns, p, True, 1.1)
+    ctx = bie.bie_create(c, a, p, mu)
+    if chunks:
+        bie.bie_set_source_chunks(ctx, chunks)
+    N = bie.bie_num_nodes(ctx)
+    F, Q = _dev(f), _dev(q)
+    rng = np.random.default_rng(ns * 7 + p)
+    tg = rng.uniform(-3, 3 + 4 * ns ** (1 / 3), (4099, 3))
+    dmin = np.min(np.linalg.norm(tg[:, None] - c[None], axis=-1) - a[None], axis=1)
+    tg = tg[np.abs(dmin) > 0.3]
+    tn = rng.standard_normal(tg.shape)
+    tn /= np.linalg.norm(tn, axis=1, keepdims=True)
+    out = {}
+    for mode in (6, 5, 5):
+        bie.bie_set_far_reduction(ctx, mode)
+        res = []
+        for excl in (0, 1):
+            bie.bie_set_near(ctx, 0.0 if excl == 0 else 0.8)
+            bie.bie_set_near_exclusion(ctx, excl)
+            u = torch.full((N, 3), np.nan, dtype=torch.float64, device="cuda")
+            bie.bie_apply_SLDL(ctx, F, Q, u)
+            res.append(u)
+        bie.bie_set_near(ctx, 0.0)
+        k = torch.full((N, 3), np.nan, dtype=torch.float64, device="cuda")
+        bie.bie_apply_K(ctx, F, k, bie.BIE_PART_FAR | bie.BIE_PART_SELF)
+        uo = torch.full((len(tg), 3), np.nan, dtype=torch.float64, device="cuda")
+        po = torch.full((len(tg),), np.nan, dtype=torch.float64, device="cuda")
+        bie.bie_eval_offsurface(ctx, F, Q, _dev(tg), uo, po)
+        to = torch.full((len(tg), 3), np.nan, dtype=torch.float64, device="cuda")
+        bie.bie_eval_traction(ctx, F, _dev(tg), _dev(tn), to)
+        torch.cuda.synchronize()
+        res += [k, uo, po, to]
+        res = [x.cpu().numpy() for x in res]
+        if mode in out:
+            assert all(np.array_equal(x, y) for x, y in zip(out[mode], res)), "chained: not deterministic"
+        out[mode] = res
+    ctx.close()
+    names = ("apply", "apply near-excluded", "K", "offsurface u", "offsurface p", "traction")
+    for x, y, what in zip(out[6], out[5], names):
+        assert np.all(np.isfinite(y)), what
+        assert np.array_equal(x + 0.0, y + 0.0), f"chained != k_reduce: {what}"
+    _assert_parity(out[5][0], oracle_mod.apply(c, a, p, mu, f, q), "chained apply")
+    uref, pref = oracle_mod.offsurface(c, a, p, mu, f, q, tg)
+    _assert_parity(out[5][3], uref, "chained off u")
+    _assert_parity(out[5][4], pref, "chained off p")

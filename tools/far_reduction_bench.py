@@ -2,7 +2,8 @@
 """Far-field schedules (bie_set_far_reduction): 0 stream-K persistent CTAs,
 1 source chunks + HBM partials + k_reduce (round 1), 2/3/4 on-chip
 thread-block-cluster reductions through distributed shared memory (clusters
-of 8/4/16).  Times bie_apply_SLDL's far
+of 8/4/16), 5 source chunks summed inside the kernel (chained, ticket order).
+FR_MODES=1,5 selects the schedules.  Times bie_apply_SLDL's far
 field (kind nbody + reduce) and the off-surface evaluator on BASELINE configs,
 L2 flushed before every timed call.  Usage: python tools/far_reduction_bench.py [cfg ...]"""
 import json
@@ -30,7 +31,7 @@ def main():
         Q = torch.from_numpy(rng.standard_normal((N, 3))).cuda()
         U = torch.empty_like(F)
         tg = torch.from_numpy(d["targets"]).cuda() if d["targets"] is not None else None
-        for mode in (0, 1, 2, 3, 4):
+        for mode in [int(x) for x in os.environ.get("FR_MODES", "0,1,2,3,4,5").split(",")]:
             bie.bie_set_far_reduction(ctx, mode)
             bie.bie_apply_SLDL(ctx, F, Q, U)
             torch.cuda.synchronize()
