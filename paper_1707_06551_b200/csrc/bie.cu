@@ -479,8 +479,9 @@ static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K, int part = 0)
   const bool stage = near_stage(c->p);
   const size_t nsm = near_smem_doubles(c->p, stage) * sizeof(double);
   const unsigned g = (unsigned)c->n_near_tgt;
+  const size_t nsm2 = near2_smem_doubles(c->p) * sizeof(double);  // PART 2, staged
   if (K && part == 2) {  // exact traction only (the smooth K sum excluded these pairs)
-    if (stage) k_near<true, true, 2><<<g, 128, nsm, s>>>(NA);
+    if (near2_stage(c->p)) k_near<true, true, 2><<<g, 128, nsm2, s>>>(NA);
     else k_near<false, true, 2><<<g, 128, nsm, s>>>(NA);
   } else if (K) {
     if (stage) k_near<true, true><<<g, 128, nsm, s>>>(NA);
@@ -489,7 +490,7 @@ static int run_near(bie_ctx* c, double* u, cudaStream_t s, bool K, int part = 0)
     if (stage) k_near<true, false, 1><<<g, 128, nsm, s>>>(NA);
     else k_near<false, false, 1><<<g, 128, nsm, s>>>(NA);
   } else if (part == 2) {  // exterior part only (measurement)
-    if (stage) k_near<true, false, 2><<<g, 128, nsm, s>>>(NA);
+    if (near2_stage(c->p)) k_near<true, false, 2><<<g, 128, nsm2, s>>>(NA);
     else k_near<false, false, 2><<<g, 128, nsm, s>>>(NA);
   } else {
     if (stage) k_near<true, false><<<g, 128, nsm, s>>>(NA);
@@ -1280,9 +1281,10 @@ int bie_create(const double* centres_h, const double* radii_h, int64_t n_spheres
   smem((const void*)k_near<false, false>, near_un);
   smem((const void*)k_near<true, false, 1>, near_st);
   smem((const void*)k_near<false, false, 1>, near_un);
-  smem((const void*)k_near<true, false, 2>, near_st);
+  const size_t near_st2 = near2_smem_doubles(p) * sizeof(double);
+  smem((const void*)k_near<true, false, 2>, near_st2);
   smem((const void*)k_near<false, false, 2>, near_un);
-  smem((const void*)k_near<true, true, 2>, near_st);
+  smem((const void*)k_near<true, true, 2>, near_st2);
   smem((const void*)k_near<false, true, 2>, near_un);
   smem((const void*)k_near<true, true>, near_st);
   smem((const void*)k_near<false, true>, near_un);

@@ -41,6 +41,24 @@ __host__ __device__ inline int64_t near_smem_doubles(int p, bool stage) {
 // stage the source sphere's records and coefficients in shared memory when they fit
 __host__ __device__ inline bool near_stage(int p) { return near_smem_doubles(p, true) * 8 <= 160 * 1024; }
 
+// PART 2 with staging: neighbours per batch -- as many coefficient blocks as
+// the record region holds, capped so that their per-node results
+// [batch][nsn][3] keep the CTA within 110 KB (two CTAs per SM, the register
+// limit) where the rest allows it, else one neighbour per batch
+__host__ __device__ inline int near2_batch(int p) {
+  const int nlm = (p + 1) * (p + 2) / 2, nsn = (p + 1) * (2 * p + 2);
+  const int b = (12 * nsn + 10 * nlm) / (10 * nlm);
+  const int64_t room = (110LL * 1024 / 8 - near_smem_doubles(p, true)) / (3LL * nsn);
+  return (int)(room < 1 ? 1 : (room < b ? room : b));
+}
+__host__ __device__ inline int64_t near2_smem_doubles(int p) {
+  const int nsn = (p + 1) * (2 * p + 2);
+  return near_smem_doubles(p, true) + 3LL * nsn * near2_batch(p);
+}
+__host__ __device__ inline bool near2_stage(int p) {
+  return near_stage(p) && near2_smem_doubles(p) * 8 <= 227 * 1024;
+}
+
 template <bool PRESSURE>
 __device__ __forceinline__ void exterior_field(int p, const double* __restrict__ cf,
                                                const double* rA, const double* rB,
@@ -75,7 +93,8 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
     // record region holds a batch of them -- two barriers per batch of B
     // neighbours instead of per neighbour (ncu r30: k_near<1,1,2> stalled on
     // barriers, 46 % FP64 pipe).  Same per-node accumulation order.
-    const int B = (12 * nsn + 10 * nlm) / (10 * nlm);
+    const int B = near2_batch(p);
+    double* res = scf + 10 * nlm;  // [B][nsn][3] per-neighbour results of the batch
     const int q0 = A.nb_off[t], q1 = A.nb_off[t + 1];
     for (int qb = q0; qb < q1; qb += B) {
       const int nb = min(B, q1 - qb);
@@ -86,7 +105,11 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
         for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
       }
       __syncthreads();
-      for (int kk = tid; kk < nsn; kk += nt) {
+      // (neighbour, node) items spread over the CTA -- nsn alone leaves lanes
+      // idle (cfg 3: 162 nodes on 128 threads, 63 % of the thread slots) --
+      // consecutive lanes on consecutive nodes of the same neighbour
+      for (int item = tid; item < nb * nsn; item += nt) {
+        const int j = item / nsn, kk = item - j * nsn;
         const int64_t i = (int64_t)t * nsn + kk;
         const double* ri = A.rec + i * kRec;
         const double xt[3] = {ri[0], ri[1], ri[2]};
@@ -96,18 +119,27 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
           nx[1] = ri[4];
           nx[2] = ri[5];
         }
+        const int s = A.nb_idx[qb + j];
+        const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+        const double a = A.radii[s];
+        const double* cfj = srec + j * 10 * nlm;
+        double ex[3];
+        if constexpr (K) exterior_traction(p, cfj, rt, rt + nlm, cs, a, xt, nx, ex);
+        else exterior_field<false>(p, cfj, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
+        double* r3 = res + 3 * item;
+        r3[0] = ex[0];
+        r3[1] = ex[1];
+        r3[2] = ex[2];
+      }
+      __syncthreads();
+      // per node, the batch's neighbours in ascending order (deterministic)
+      for (int kk = tid; kk < nsn; kk += nt) {
         double d0 = du[3 * kk], d1 = du[3 * kk + 1], d2 = du[3 * kk + 2];
         for (int j = 0; j < nb; ++j) {
-          const int s = A.nb_idx[qb + j];
-          const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
-          const double a = A.radii[s];
-          const double* cfj = srec + j * 10 * nlm;
-          double ex[3];
-          if constexpr (K) exterior_traction(p, cfj, rt, rt + nlm, cs, a, xt, nx, ex);
-          else exterior_field<false>(p, cfj, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
-          d0 += ex[0] - 0.0;
-          d1 += ex[1] - 0.0;
-          d2 += ex[2] - 0.0;
+          const double* r3 = res + 3 * (j * nsn + kk);
+          d0 += r3[0];
+          d1 += r3[1];
+          d2 += r3[2];
         }
         du[3 * kk] = d0;
         du[3 * kk + 1] = d1;
