@@ -94,6 +94,35 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   for (int sp = 0; sp < SPC; ++sp) {
     sidx[sp] = (int64_t)blockIdx.x * SPC + sp;
     valid[sp] = sidx[sp] < A.ns;
+  }
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // f and q of the sphere (contiguous 24 nsn bytes each) land in F through the
+  // TMA unit (cp.async.bulk, no LSU wavefronts); the strided per-node reads of
+  // phase A and of the record writer then hit shared memory (ncu r18: the
+  // kernel was bound by L1 wavefronts, 84 %, half of them strided global
+  // accesses).  Unaligned user pointers fall back to cooperative loads.  The
+  // copies are issued first so that their DRAM latency overlaps the rest of
+  // the CTA's set-up; the other threads meet the mbarrier only after the
+  // barrier below.
+  const bool tma_f = A.f && !(reinterpret_cast<uintptr_t>(A.f) & 15);
+  const bool tma_q = A.q && !(reinterpret_cast<uintptr_t>(A.q) & 15);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = (uint32_t)(3 * nsn * sizeof(double));
+    int nvalid = 0;
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp) nvalid += valid[sp] ? 1 : 0;
+    mbar_arrive_expect_tx(bar, (uint32_t)nvalid * bytes * ((tma_f ? 1 : 0) + (tma_q ? 1 : 0)));
+#pragma unroll
+    for (int sp = 0; sp < SPC; ++sp) {
+      if (!valid[sp]) continue;
+      if (tma_f) bulk_g2s(Fp_(sp), A.f + sidx[sp] * 3 * nsn, bytes, bar);
+      if (tma_q) bulk_g2s(Fp_(sp) + 3 * nsn, A.q + sidx[sp] * 3 * nsn, bytes, bar);
+    }
+  }
+#pragma unroll
+  for (int sp = 0; sp < SPC; ++sp) {
     const int64_t sc = valid[sp] ? sidx[sp] : A.ns - 1;
     ra[sp] = A.radii[sc];
     rcx[sp] = A.centres[3 * sc];
@@ -102,7 +131,6 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     raS[sp] = ra[sp] / A.mu;
   }
   const double cS = 1.0 / (8.0 * kPi * A.mu), cD = 3.0 / (4.0 * kPi);
-  const int tid = threadIdx.x, nt = blockDim.x;
 
   // ---------------------------------------------------------------- A (+ B0)
   // Node pairs (k, nphi-k) of a latitude are handled by one thread so that
@@ -140,17 +168,6 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     g[5] = -q0 * sp_ + q1 * cp;
   };
   // -------------------------------------------------------------- A0 staging
-  // f and q of the sphere (contiguous 24 nsn bytes each) land in F through the
-  // TMA unit (cp.async.bulk, no LSU wavefronts); the strided per-node reads of
-  // phase A and of the record writer then hit shared memory (ncu r18: the
-  // kernel was bound by L1 wavefronts, 84 %, half of them strided global
-  // accesses).  Unaligned user pointers fall back to cooperative loads.
-  const bool tma_f = A.f && !(reinterpret_cast<uintptr_t>(A.f) & 15);
-  const bool tma_q = A.q && !(reinterpret_cast<uintptr_t>(A.q) & 15);
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
   for (int k = tid; k < nphi; k += nt) tw[k] = make_double2(tab[L.cph + k], tab[L.sph + k]);
 #pragma unroll
   for (int sp = 0; sp < SPC; ++sp) {
@@ -162,19 +179,6 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     }
   }
   __syncthreads();  // tw, fallback staging and the mbarrier ready
-  if (tid == 0) {
-    const uint32_t bytes = (uint32_t)(3 * nsn * sizeof(double));
-    int nvalid = 0;
-#pragma unroll
-    for (int sp = 0; sp < SPC; ++sp) nvalid += valid[sp] ? 1 : 0;
-    mbar_arrive_expect_tx(bar, (uint32_t)nvalid * bytes * ((tma_f ? 1 : 0) + (tma_q ? 1 : 0)));
-#pragma unroll
-    for (int sp = 0; sp < SPC; ++sp) {
-      if (!valid[sp]) continue;
-      if (tma_f) bulk_g2s(Fp_(sp), A.f + sidx[sp] * 3 * nsn, bytes, bar);
-      if (tma_q) bulk_g2s(Fp_(sp) + 3 * nsn, A.q + sidx[sp] * 3 * nsn, bytes, bar);
-    }
-  }
   mbar_wait(bar, 0);
   // -------------------------------------------------------------- A1 records
   // Without out_stage (shared memory too small): packed source records (row
@@ -343,7 +347,9 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // ---------------------------------------------------------------- C2
   // {Y,G,X} -> {V,W,X} (eqs 2.13-2.14), diagonal scale (Thm 2), back to
   // {Y,G,X} (eqs 2.16-2.17) for the inverse transform.
-  for (int c = tid; c < nlm; c += nt) {
+  // items (c, re/im): twice the column count, so that more threads have work
+  for (int itc = tid; itc < 2 * nlm; itc += nt) {
+    const int c = itc >> 1, ri = itc & 1;
     int m = 0, off = 0;
     while (off + (P1 - m) <= c) { off += P1 - m; ++m; }
     const int n = m + (c - off);
@@ -358,8 +364,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
       const double* aq = ALPHA + 6 * (nlm + c);
       double* o = Fp_(sp) + 6 * c;  // PSI
       const double aS = raS[sp];
-#pragma unroll
-      for (int ri = 0; ri < 2; ++ri) {
+      {
         double aV[2], aW[2], aX[2];
         const double* al[2] = {af, aq};
 #pragma unroll
