@@ -432,6 +432,7 @@ static SelfArgs self_args(const bie_ctx* c, const double* f, const double* q, do
   SA.p = c->p;
   SA.ns = c->ns;
   SA.mu = c->mu;
+  SA.cS = 1.0 / (8.0 * kPi * c->mu);
   SA.tab = c->d_tab;
   SA.centres = c->d_centres;
   SA.radii = c->d_radii;

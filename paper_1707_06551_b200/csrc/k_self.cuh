@@ -43,9 +43,23 @@ struct SelfArgs {
   int precond;      // 1: u = P^{-1} q with P = 1/2 I + S_self + D_self (f ignored):
                     //    eigenvalue 1/(1/2 + lamS a/mu + lamD) on every VSH mode of
                     //    degree <= p and 2 on the rest (NEXT-2 preconditioner)
+  double cS = 0.0;    // 1/(8 pi mu) (computed once on the host)
   int out_stage = 0;  // k_self_t: records (and u) staged in shared memory and written
                       // by TMA bulk stores (launch with self_smem_bytes(p, SPC, true))
 };
+
+
+// column c of the m-major (n, m) layout (lm_index) -> m and the column of
+// (m, m): the root of off(m) = m P1 - m (m - 1) / 2 <= c in fp32, then one
+// integer correction step each way (exact for every p <= BIE_P_MAX)
+__device__ __forceinline__ void decode_col(int c, int P1, int& m, int& off) {
+  const float b = 2.0f * P1 + 1.0f;
+  m = (int)((b - sqrtf(b * b - 8.0f * c)) * 0.5f);
+  m = max(0, min(m, P1 - 1));
+  off = m * P1 - (m * (m - 1)) / 2;
+  if (off > c) { --m; off -= P1 - m; }
+  else if (off + (P1 - m) <= c) { off += P1 - m; ++m; }
+}
 
 __host__ __device__ inline int64_t self_smem_doubles(int p);
 // Dynamic shared memory of k_self_t for SPC spheres per CTA; out_stage adds
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
     rcz[sp] = A.centres[3 * sc + 2];
     raS[sp] = ra[sp] / A.mu;
   }
-  const double cS = 1.0 / (8.0 * kPi * A.mu), cD = 3.0 / (4.0 * kPi);
+  const double cS = A.cS, cD = 3.0 / (4.0 * kPi);  // cS = 1/(8 pi mu) from the host
 
   // ---------------------------------------------------------------- A (+ B0)
   // Node pairs (k, nphi-k) of a latitude are handled by one thread so that
@@ -302,8 +316,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // complex.  ALPHA aliases C, which is dead after phase B.
   for (int it = tid; it < 2 * nlm; it += nt) {
     const int d = it / nlm, c = it - d * nlm;
-    int m = 0, off = 0;
-    while (off + (P1 - m) <= c) { off += P1 - m; ++m; }
+    int m, off;
+    decode_col(c, P1, m, off);
     double y0[SPC], y1[SPC], g0[SPC], g1[SPC], x0[SPC], x1[SPC];
 #pragma unroll
     for (int sp = 0; sp < SPC; ++sp) y0[sp] = y1[sp] = g0[sp] = g1[sp] = x0[sp] = x1[sp] = 0.0;
@@ -350,13 +364,12 @@ __global__ void __launch_bounds__(TPB, MINB) k_self_t(SelfArgs A) {
   // items (c, re/im): twice the column count, so that more threads have work
   for (int itc = tid; itc < 2 * nlm; itc += nt) {
     const int c = itc >> 1, ri = itc & 1;
-    int m = 0, off = 0;
-    while (off + (P1 - m) <= c) { off += P1 - m; ++m; }
+    int m, off;
+    decode_col(c, P1, m, off);
     const int n = m + (c - off);
     const double* lS = tab + L.lamS + 3 * n;
     const double* lD = tab + L.lamD + 3 * n;
-    const double inn = n ? 1.0 / ((double)n * (n + 1)) : 0.0;
-    const double i2n = 1.0 / (2.0 * n + 1.0);
+    const double inn = tab[L.cinv + 2 * n], i2n = tab[L.cinv + 2 * n + 1];  // (table: no divisions)
 #pragma unroll
     for (int sp = 0; sp < SPC; ++sp) {
       const double* ALPHA = Cp(sp);

@@ -10,7 +10,7 @@ namespace bie {
 struct TableLayout {
   int p, nphi, nlm;  // nlm = (p+1)(p+2)/2 (n,m) pairs with m >= 0
   // offsets in doubles
-  int64_t t, st, wu, cph, sph, P, dP, mPs, lamS, lamD, rA, rB, rC, total;
+  int64_t t, st, wu, cph, sph, P, dP, mPs, lamS, lamD, rA, rB, rC, cinv, total;
   __host__ __device__ explicit TableLayout(int p_) : p(p_) {
     nphi = 2 * p + 2;
     nlm = (p + 1) * (p + 2) / 2;
@@ -29,6 +29,7 @@ struct TableLayout {
     rA = o;   o += nlm;  // normalised-Legendre recurrence coefficients per (n, m):
     rB = o;   o += nlm;  //   P~_n = rA (t P~_{n-1} - rB P~_{n-2})
     rC = o;   o += nlm;  //   sin(th) dP~_n/dth = n t P~_n - rC P~_{n-1}
+    cinv = o; o += 2 * (p + 1);  // per degree n: 1/(n(n+1)) (0 at n = 0), 1/(2n+1)
     total = o;
   }
 };
@@ -99,6 +100,8 @@ __global__ void k_tables(int p, double* tab) {
     lD[1] = n ? -1.5 / (a * (2.0 * n - 1.0)) : 0.0;
     lS[2] = n ? 1.0 / a : 0.0;                 // X (X_0 = 0)
     lD[2] = n ? -1.5 / a : 0.0;
+    tab[L.cinv + 2 * n] = n ? 1.0 / ((double)n * (n + 1)) : 0.0;  // eqs 2.13-2.14 factors
+    tab[L.cinv + 2 * n + 1] = 1.0 / (2.0 * n + 1.0);
   }
   if (tid >= (p + 1) * (p + 1)) return;
   const int j = tid / (p + 1), m = tid % (p + 1);
