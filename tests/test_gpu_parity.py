@@ -500,6 +500,10 @@ def test_chained_reduction_matches_k_reduce(bie, oracle_mod, ns, p, chunks):
         if mode in out:
             assert all(np.array_equal(x, y) for x, y in zip(out[mode], res)), "chained: not deterministic"
         out[mode] = res
+    for bad in (-1, 7):
+        with pytest.raises(bie.BieError) as e:
+            bie.bie_set_far_reduction(ctx, bad)
+        assert e.value.status == bie.BIE_ERR_ARG
     ctx.close()
     names = ("apply", "apply near-excluded", "K", "offsurface u", "offsurface p", "traction")
     for x, y, what in zip(out[6], out[5], names):
