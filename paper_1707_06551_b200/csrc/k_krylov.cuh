@@ -55,20 +55,41 @@ __global__ void __launch_bounds__(kDotThreads) k_dot_final(const double* __restr
 
 namespace bie {
 
-// part[i][b] = block b's partial of  V_i . w,  i < nv   (fixed grid)
+// part[i][b] = block b's partial of  V_i . w,  i < nv   (fixed grid).  Four
+// vectors per pass share the loads of w and one barrier; each partial is
+// reduced exactly as block_sum does (per-thread fma chain, warp xor tree,
+// then warp q's xor tree over the warp sums of vector q), so the values are
+// those of one block_sum per vector.
 __global__ void __launch_bounds__(kDotThreads) k_mdot_partial(int64_t n, int nv,
                                                               const double* __restrict__ V,
                                                               const double* __restrict__ w,
                                                               double* __restrict__ part) {
-  __shared__ double red[kDotThreads / 32];
-  for (int i = 0; i < nv; ++i) {
-    const double* v = V + (int64_t)i * n;
-    double s = 0.0;
+  constexpr int NW = kDotThreads / 32, G = 4;
+  static_assert(NW >= G, "one warp per vector of a group");
+  __shared__ double red[G][NW];
+  const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int i0 = 0; i0 < nv; i0 += G) {
+    const int g = min(G, nv - i0);
+    double s[G] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t e = blockIdx.x * (int64_t)kDotThreads + threadIdx.x; e < n;
-         e += (int64_t)kDotBlocks * kDotThreads)
-      s = fma(v[e], w[e], s);
-    s = block_sum(s, red);
-    if (threadIdx.x == 0) part[(int64_t)i * kDotBlocks + blockIdx.x] = s;
+         e += (int64_t)kDotBlocks * kDotThreads) {
+      const double we = w[e];
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+        if (q < g) s[q] = fma(V[(int64_t)(i0 + q) * n + e], we, s[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      double v = s[q];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (l == 0) red[q][wi] = v;
+    }
+    __syncthreads();
+    if (wi < g) {
+      double v = l < NW ? red[wi][l] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (l == 0) part[(int64_t)(i0 + wi) * kDotBlocks + blockIdx.x] = v;
+    }
     __syncthreads();
   }
 }
