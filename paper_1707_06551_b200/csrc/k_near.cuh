@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
   const int t = A.tgt[blockIdx.x];
   for (int e = tid; e < 3 * nlm; e += nt) rt[e] = A.tab[L.rA + e];
   for (int e = tid; e < 3 * nsn; e += nt) du[e] = 0.0;
-  if (PART == 2 && STAGE) {
+  if constexpr (PART == 2 && STAGE) {
     // Exterior part alone: only the neighbours' coefficients are read, so the
     // record region holds a batch of them -- two barriers per batch of B
     // neighbours instead of per neighbour (ncu r30: k_near<1,1,2> stalled on
@@ -149,60 +149,61 @@ __global__ void __launch_bounds__(128) k_near(const NearArgs A) {
     __syncthreads();
     for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
     return;
-  }
-  for (int qn = A.nb_off[t]; qn < A.nb_off[t + 1]; ++qn) {
-    const int s = A.nb_idx[qn];
-    const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
-    const double a = A.radii[s];
-    const double* cf = A.coef + (int64_t)s * nlm * 10;
-    const double* rec_s = A.rec + (int64_t)s * nsn * kRec;
-    if (STAGE) {
-      __syncthreads();  // previous neighbour's staged data no longer in use
-      if (PART != 2) {  // (the exterior part alone needs only the coefficients)
-        const double2* g2 = reinterpret_cast<const double2*>(rec_s);
-        double2* s2 = reinterpret_cast<double2*>(srec);
-        for (int e = tid; e < 6 * nsn; e += nt) s2[e] = g2[e];
-        rec_s = srec;
+  } else {  // the general path (not compiled where the branch above returns)
+    for (int qn = A.nb_off[t]; qn < A.nb_off[t + 1]; ++qn) {
+      const int s = A.nb_idx[qn];
+      const double cs[3] = {A.centres[3 * s], A.centres[3 * s + 1], A.centres[3 * s + 2]};
+      const double a = A.radii[s];
+      const double* cf = A.coef + (int64_t)s * nlm * 10;
+      const double* rec_s = A.rec + (int64_t)s * nsn * kRec;
+      if (STAGE) {
+        __syncthreads();  // previous neighbour's staged data no longer in use
+        if (PART != 2) {  // (the exterior part alone needs only the coefficients)
+          const double2* g2 = reinterpret_cast<const double2*>(rec_s);
+          double2* s2 = reinterpret_cast<double2*>(srec);
+          for (int e = tid; e < 6 * nsn; e += nt) s2[e] = g2[e];
+          rec_s = srec;
+        }
+        const double2* c2 = reinterpret_cast<const double2*>(cf);
+        double2* d2 = reinterpret_cast<double2*>(scf);
+        for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
+        __syncthreads();
+        cf = scf;
+      } else if (qn == A.nb_off[t]) {
+        __syncthreads();
       }
-      const double2* c2 = reinterpret_cast<const double2*>(cf);
-      double2* d2 = reinterpret_cast<double2*>(scf);
-      for (int e = tid; e < 5 * nlm; e += nt) d2[e] = c2[e];
-      __syncthreads();
-      cf = scf;
-    } else if (qn == A.nb_off[t]) {
-      __syncthreads();
-    }
-    const double2* sr = reinterpret_cast<const double2*>(rec_s);
-    for (int kk = tid; kk < nsn; kk += nt) {
-      const int64_t i = (int64_t)t * nsn + kk;
-      const double* ri = A.rec + i * kRec;
-      const double xt[3] = {ri[0], ri[1], ri[2]};
-      double ex[3], acc[3] = {0.0, 0.0, 0.0};
-      if constexpr (K) {
-        const double nx[3] = {ri[3], ri[4], ri[5]};
-        exterior_traction(p, cf, rt, rt + nlm, cs, a, xt, nx, ex);
-        if (PART != 2)
-          for (int k = 0; k < nsn; ++k) {
-            const double2* q2 = sr + k * (kRec / 2);
-            pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
-          }
-      } else {
-        ex[0] = ex[1] = ex[2] = 0.0;
-        if (PART != 1) exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
-        double pdummy = 0.0;
-        if (PART != 2)
-          for (int k = 0; k < nsn; ++k) {
-            const double2* q2 = sr + k * (kRec / 2);
-            pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
-          }
+      const double2* sr = reinterpret_cast<const double2*>(rec_s);
+      for (int kk = tid; kk < nsn; kk += nt) {
+        const int64_t i = (int64_t)t * nsn + kk;
+        const double* ri = A.rec + i * kRec;
+        const double xt[3] = {ri[0], ri[1], ri[2]};
+        double ex[3], acc[3] = {0.0, 0.0, 0.0};
+        if constexpr (K) {
+          const double nx[3] = {ri[3], ri[4], ri[5]};
+          exterior_traction(p, cf, rt, rt + nlm, cs, a, xt, nx, ex);
+          if (PART != 2)
+            for (int k = 0; k < nsn; ++k) {
+              const double2* q2 = sr + k * (kRec / 2);
+              pair_K<false>(q2[0], q2[1], q2[4], q2[5], xt, nx, acc, 0, 0, 1);
+            }
+        } else {
+          ex[0] = ex[1] = ex[2] = 0.0;
+          if (PART != 1) exterior_field<false>(p, cf, rt, rt + nlm, rt + 2 * nlm, cs, a, xt, ex, nullptr);
+          double pdummy = 0.0;
+          if (PART != 2)
+            for (int k = 0; k < nsn; ++k) {
+              const double2* q2 = sr + k * (kRec / 2);
+              pair_acc<false, false>(q2[0], q2[1], q2[2], q2[3], q2[4], q2[5], 0.0, xt, acc, pdummy, 0, 0, 1);
+            }
+        }
+        du[3 * kk + 0] += ex[0] - acc[0];
+        du[3 * kk + 1] += ex[1] - acc[1];
+        du[3 * kk + 2] += ex[2] - acc[2];
       }
-      du[3 * kk + 0] += ex[0] - acc[0];
-      du[3 * kk + 1] += ex[1] - acc[1];
-      du[3 * kk + 2] += ex[2] - acc[2];
     }
+    __syncthreads();
+    for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
   }
-  __syncthreads();
-  for (int e = tid; e < 3 * nsn; e += nt) A.u[(int64_t)t * 3 * nsn + e] += du[e];
 }
 
 }  // namespace bie
