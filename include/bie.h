@@ -376,9 +376,22 @@ int bie_set_self_kernel(bie_ctx* ctx, int variant);
  *   the 8 / 4 / 16 source chunks of a target tile run as ONE thread-block
  *   cluster (16: apply only, non-portable size) and are summed on chip through
  *   distributed shared memory in fixed rank order; smaller launches use 1.
+ * 7: constant-bank batches (SL+DL apply without near exclusion, off-surface
+ *   u / p; other far-field operators keep schedule 1).  The sources are cut
+ *   into batches of 312 records that are copied device-to-device into one of
+ *   two __constant__ buffers; one launch per batch adds the batch's
+ *   contribution at every target to an accumulator.  The FP64 instructions
+ *   then take the source operands from the uniform datapath instead of the
+ *   vector register file, which lifts the register-file read limit of the
+ *   shared-memory kernel.  Even batches run on the caller's
+ *   stream into u, odd batches on a stream owned by the context into scratch
+ *   ([M][3] (+ [M]) doubles), joined before the call's work on the caller's
+ *   stream ends; the two partial sums are added at the end.  The constant
+ *   buffers belong to the process: passes of different contexts on one device
+ *   are ordered one after the other by an event.
  * bie_set_source_chunks > 0 forces the chunked schedules (1, 5 or 6).  All
  * schedules are deterministic; they differ only in fp64 summation grouping
- * (1, 5 and 6 not at all).  BIE_ERR_ARG outside 0..6.
+ * (1, 5 and 6 not at all).  BIE_ERR_ARG outside 0..7.
  */
 int bie_set_far_reduction(bie_ctx* ctx, int mode);
 

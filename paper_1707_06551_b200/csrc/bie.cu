@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <algorithm>
 #include <unordered_map>
@@ -19,6 +20,7 @@
 #include "k_complete.cuh"
 #include "k_krylov.cuh"
 #include "k_nbody.cuh"
+#include "k_nbody_c.cuh"
 #include "k_n4.cuh"
 #include "k_near.cuh"
 #include "k_self.cuh"
@@ -37,6 +39,7 @@ namespace {
 // registers -- pressure, normals -- make 8 spill-prone and RF-read bound).
 constexpr int kTPB = 64, kTS = 64, kNST = 3;
 constexpr int kR_APPLY = 8, kR_OFF = 7, kR_K = 7, kR_OFFK = 7;
+constexpr int kR_APPLY_C = 8, kR_OFF_C = 8, kUNR_C = 4;  // constant-bank kernels (k_nbody_c.cuh)
 constexpr int64_t kOffBatch = 1 << 21;  // off-surface targets per batch (bounds scratch)
 constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 
@@ -83,6 +86,8 @@ struct bie_ctx {
   double* d_qn3 = nullptr;
   double* d_part = nullptr;
   size_t part_cap = 0;  // doubles
+  cudaStream_t st_side = nullptr;              // constant-bank far field: stream of the odd batches
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* d_sht = nullptr;  // fragment-order transform tables of k_sht
   int sht_occ = 1;          // resident k_sht CTAs per SM
   int self_variant = -1;    // -1 auto (fastest measured per order), 0 k_sht DMMA, 1 k_sht DFMA,
@@ -845,7 +850,78 @@ static int run_sk(bie_ctx* c, Kern kern, Fix fix, int which, int r, int nc, Nbod
 }
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
+
+// Constant-bank far field (bie_set_far_reduction 7; k_nbody_c.cuh): batches of
+// kCB sources, even batches on the caller's stream into `acc` (which already
+// holds the self term / zeros), odd batches on the context's side stream into
+// the scratch accumulator, joined by k_nbody_c_join.  The two constant buffers
+// belong to the process's CUDA module, not to a context: passes of different
+// contexts on one device are ordered one after the other by an event (the
+// enqueue runs under a mutex), so distinct contexts stay independent.
+static std::mutex g_cb_mu;
+static cudaEvent_t g_cb_done[64] = {};
+
+template <bool OFF>
+static int run_const_pass(bie_ctx* c, const double* tx, int64_t M, double* acc, double* pout, int kind,
+                          cudaStream_t s) {
+  constexpr int R = OFF ? kR_OFF_C : kR_APPLY_C;
+  Ev ev;
+  int rc;
+  if (c->dev < 0 || c->dev >= 64) return fail(c, BIE_ERR_UNSUPPORTED, "constant-bank far field: device index%s");
+  if (!c->st_side) {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->st_side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(c, e, "constant-bank far field: side stream");
+  }
+  const bool wp = OFF && pout != nullptr;
+  if ((rc = ensure_part(c, (size_t)(wp ? 4 : 3) * M))) return rc;
+  double* accB = c->d_part;
+  double* pB = wp ? c->d_part + 3 * M : nullptr;
+  const int64_t nb = (c->N + kCB - 1) / kCB;
+  const unsigned grid = (unsigned)((M + (int64_t)kTPB * R - 1) / ((int64_t)kTPB * R));
+  std::lock_guard<std::mutex> lk(g_cb_mu);
+  cudaEvent_t& done = g_cb_done[c->dev];
+  cudaError_t e = cudaSuccess;
+  if (!done) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  else e = cudaStreamWaitEvent(s, done, 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "constant-bank far field: ordering event");
+  prof_begin(c, kind, s, &ev);
+  cudaMemsetAsync(accB, 0, (size_t)(wp ? 4 : 3) * M * sizeof(double), s);
+  cudaEventRecord(c->ev_fork, s);
+  cudaStreamWaitEvent(c->st_side, c->ev_fork, 0);
+  for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
+    const int w = (int)(b & 1);
+    cudaStream_t sb = w ? c->st_side : s;
+    NbodyCArgs A;
+    A.tx = tx;
+    A.acc = w ? accB : acc;
+    A.pacc = wp ? (w ? pB : pout) : nullptr;
+    A.M = M;
+    A.k0 = b * kCB;
+    A.ks = (int)std::min<int64_t>(kCB, c->N - A.k0);
+    A.nsn = c->nsn;
+    e = cudaMemcpyToSymbolAsync(c_nb_rec, c->d_rec + A.k0 * kRec, (size_t)A.ks * kRec * sizeof(double),
+                                (size_t)w * kCB * kRec * sizeof(double), cudaMemcpyDeviceToDevice, sb);
+    if (e == cudaSuccess && OFF)
+      e = cudaMemcpyToSymbolAsync(c_nb_qn, c->d_qn3 + A.k0, (size_t)A.ks * sizeof(double),
+                                  (size_t)w * kCB * sizeof(double), cudaMemcpyDeviceToDevice, sb);
+    if (e != cudaSuccess) break;
+    if (w) k_nbody_c<R, kTPB, kUNR_C, 1, OFF><<<grid, kTPB, 0, sb>>>(A);
+    else k_nbody_c<R, kTPB, kUNR_C, 0, OFF><<<grid, kTPB, 0, sb>>>(A);
+  }
+  cudaEventRecord(c->ev_join, c->st_side);
+  cudaStreamWaitEvent(s, c->ev_join, 0);
+  k_nbody_c_join<<<(unsigned)((3 * M + 255) / 256), 256, 0, s>>>(M, acc, accB, wp ? pout : nullptr, pB, 2.0 * c->mu);
+  prof_end(c, s, &ev);
+  cudaEventRecord(done, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "constant-bank far field: batch copy");
+  return launch_check(c, OFF ? "k_nbody_c (off-surface)" : "k_nbody_c");
+}
+
 static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode, bool nx) {
+  if (c->far_red == 7 && mode == 0 && !nx && c->chunks_override == 0)
+    return run_const_pass<false>(c, c->d_x, c->N, u, nullptr, BIE_KIND_NBODY, s);
   Ev ev;
   int rc;
   const ChunkPlan P = plan_chunks(c, c->N, c->N,
@@ -982,6 +1058,13 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
   for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
     const int64_t Mb = std::min(kOffBatch, m - b0);
+    if (c->far_red == 7 && c->chunks_override == 0) {  // constant-bank batches (k_nbody_c.cuh)
+      cudaMemsetAsync(u + 3 * b0, 0, (size_t)3 * Mb * sizeof(double), s);
+      if (p) cudaMemsetAsync(p + b0, 0, (size_t)Mb * sizeof(double), s);
+      if ((rc = run_const_pass<true>(c, tg + 3 * b0, Mb, u + 3 * b0, p ? p + b0 : nullptr, BIE_KIND_OFFSURF, s)))
+        return rc;
+      continue;
+    }
     const ChunkPlan P = plan_chunks(c, Mb, c->N, c->occ_off, kR_OFF);
     NbodyArgs A;
     A.rec = c->d_rec;
@@ -1178,6 +1261,9 @@ void bie_destroy(bie_ctx* c) {
   if (c->d_delta) cudaFree(c->d_delta);
   if (c->d_deltaT) cudaFree(c->d_deltaT);
   if (c->d_psinear) cudaFree(c->d_psinear);
+  if (c->st_side) cudaStreamDestroy(c->st_side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   cudaFree(c->d_cacc);
   cudaFree(c->d_chain);
   cudaFree(c->d_cell_start);
@@ -1987,7 +2073,7 @@ int bie_solve_porous(bie_ctx* c, const double* uinf, double* mu_out, double tol,
 
 int bie_set_far_reduction(bie_ctx* c, int mode) {
   if (!c) return BIE_ERR_ARG;
-  if (mode < 0 || mode > 6) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..6%s");
+  if (mode < 0 || mode > 7) return fail(c, BIE_ERR_ARG, "far reduction mode must be 0..7%s");
   c->far_red = mode;
   return BIE_OK;
 }

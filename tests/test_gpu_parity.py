@@ -406,7 +406,7 @@ def test_far_schedules_agree(bie, oracle_mod):
     N = F.shape[0]
     tg = _dev(d["targets"][:600000])
     out = {}
-    for mode in (0, 1, 2, 5, 6, 0):
+    for mode in (0, 1, 2, 5, 6, 7, 7, 0):
         bie.bie_set_far_reduction(ctx, mode)
         u = torch.empty((N, 3), dtype=torch.float64, device="cuda")
         bie.bie_apply_SLDL(ctx, F, Q, u)
@@ -423,7 +423,7 @@ def test_far_schedules_agree(bie, oracle_mod):
     ctx.close()
     for m in (5, 6):  # the default (1) chains at this size; 5 always, 6 never: same sums
         assert all(np.array_equal(a + 0.0, b + 0.0) for a, b in zip(out[1], out[m])), ("chained", m)
-    for m in (1, 2):
+    for m in (1, 2, 7):  # 7: constant-bank batches (apply and off-surface; K keeps the default)
         for a, b, what in zip(out[0], out[m], ("apply", "offsurface u", "offsurface p", "K")):
             rel, mx = _err(a, b)
             assert rel <= 1e-13 and mx <= 1e-12, (m, what, rel, mx)
@@ -455,6 +455,52 @@ def test_stream_k_small_and_ragged(bie, oracle_mod, ns, p):
     ctx.close()
     _assert_parity(u.cpu().numpy(), uref, "sk off u")
     _assert_parity(pr.cpu().numpy(), pref, "sk off p")
+
+
+@pytest.mark.parametrize("ns,p", [(1, 3), (2, 1), (3, 4), (7, 6), (40, 5), (12, 8), (5, 12)])
+def test_constant_bank_far_field(bie, oracle_mod, ns, p):
+    """bie_set_far_reduction(7): sources as constant-bank operands in batches of
+    312 records over two streams (k_nbody_c.cuh).  Apply (self-sphere exclusion
+    in batches that straddle spheres, one batch only, ragged last batch and
+    target tile) and off-surface u / p against the oracle; deterministic; a
+    second context used in between must not disturb the first (the constant
+    buffers are shared by the process)."""
+    c, a, f, q, mu = _random_case(1500 + ns + p, ns, p, True, 1.2)
+    ctx = bie.bie_create(c, a, p, mu)
+    ctx2 = bie.bie_create(c[:1] + 100.0, a[:1], p, mu)
+    bie.bie_set_far_reduction(ctx, 7)
+    bie.bie_set_far_reduction(ctx2, 7)
+    N = bie.bie_num_nodes(ctx)
+    n1 = bie.bie_num_nodes(ctx2)
+    F, Q = _dev(f), _dev(q)
+    rng = np.random.default_rng(ns + 31)
+    tg = rng.uniform(-3, 3 + 4 * ns ** (1 / 3), (3001, 3))
+    dmin = np.min(np.linalg.norm(tg[:, None] - c[None], axis=-1) - a[None], axis=1)
+    tg = tg[np.abs(dmin) > 0.3]
+    s2 = torch.cuda.Stream()
+    res = []
+    for rep in range(2):
+        ua = torch.full((N, 3), np.nan, dtype=torch.float64, device="cuda")
+        bie.bie_apply_SLDL(ctx, F, Q, ua)
+        with torch.cuda.stream(s2):  # another context, another stream, same constant buffers
+            u2 = torch.full((n1, 3), np.nan, dtype=torch.float64, device="cuda")
+            bie.bie_apply_SLDL(ctx2, F[:n1].clone(), Q[:n1].clone(), u2)
+        u = torch.full((len(tg), 3), np.nan, dtype=torch.float64, device="cuda")
+        pr = torch.full((len(tg),), np.nan, dtype=torch.float64, device="cuda")
+        bie.bie_eval_offsurface(ctx, F, Q, _dev(tg), u, pr)
+        uv = torch.full((len(tg), 3), np.nan, dtype=torch.float64, device="cuda")
+        bie.bie_eval_offsurface(ctx, F, Q, _dev(tg), uv, None)
+        torch.cuda.synchronize()
+        res.append([x.cpu().numpy() for x in (ua, u, pr, uv)])
+    ctx.close()
+    ctx2.close()
+    assert all(np.array_equal(x, y) for x, y in zip(res[0], res[1])), "constant-bank: not deterministic"
+    ua, u, pr, uv = res[0]
+    assert np.array_equal(u, uv), "velocity depends on the pressure output"
+    _assert_parity(ua, oracle_mod.apply(c, a, p, mu, f, q), f"const apply {ns}")
+    uref, pref = oracle_mod.offsurface(c, a, p, mu, f, q, tg)
+    _assert_parity(u, uref, "const off u")
+    _assert_parity(pr, pref, "const off p")
 
 
 @pytest.mark.parametrize("ns,p,chunks", [(3, 4, 2), (7, 6, 3), (40, 5, 7), (12, 8, 0), (2, 1, 2)])
@@ -500,7 +546,7 @@ def test_chained_reduction_matches_k_reduce(bie, oracle_mod, ns, p, chunks):
         if mode in out:
             assert all(np.array_equal(x, y) for x, y in zip(out[mode], res)), "chained: not deterministic"
         out[mode] = res
-    for bad in (-1, 7):
+    for bad in (-1, 8):
         with pytest.raises(bie.BieError) as e:
             bie.bie_set_far_reduction(ctx, bad)
         assert e.value.status == bie.BIE_ERR_ARG

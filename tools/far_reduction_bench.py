@@ -2,7 +2,8 @@
 """Far-field schedules (bie_set_far_reduction): 0 stream-K persistent CTAs,
 1 source chunks + HBM partials + k_reduce (round 1), 2/3/4 on-chip
 thread-block-cluster reductions through distributed shared memory (clusters
-of 8/4/16), 5 source chunks summed inside the kernel (chained, ticket order).
+of 8/4/16), 5 source chunks summed inside the kernel (chained, ticket order),
+7 constant-bank source batches over two streams (k_nbody_c.cuh).
 FR_MODES=1,5 selects the schedules.  Times bie_apply_SLDL's far
 field (kind nbody + reduce) and the off-surface evaluator on BASELINE configs,
 L2 flushed before every timed call.  Usage: python tools/far_reduction_bench.py [cfg ...]"""
