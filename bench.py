@@ -291,6 +291,7 @@ def run_gpu(args):
              "algorithmic_bytes": rec_bytes + tgt_bytes,
              "traffic_source": (tr or {}).get("source"),
              "kernel": kname, "ms_per_launch_avg": round(ms / max(prof[kind][1] / args.steps, 1), 4),
+             "ms_per_pass": round(ms, 4), "launches_per_pass": prof[kind][1] / args.steps,
              "pairs_per_s": pairs_s, "flops_per_pair": flops_per_pair,
              "peak_source": peak_src + " (of measured)",
              "fp64_pipe_frac_at_max_clock": round(pairs_s * ops_per_pair /
@@ -301,16 +302,27 @@ def run_gpu(args):
         return r
 
     # dominant kernel of the headline: the apply's far-field pair sum (k_nbody)
+    # Large launches (cfg 4, 5) run the constant-bank schedule: one far-field pass =
+    # one launch of k_nbody_c per batch of 312 sources, alternating between two
+    # streams (their launches overlap), plus the join; the pass is timed as a whole
+    # by the ABI's events on the launching stream, and "achieved" = the pass's
+    # algorithmic flops / that time (ms_per_pass; ms_per_launch_avg = pass time /
+    # launches, the effective time per launch).
+    const_a = prof["nbody"][1] / args.steps > 8
     roofline = kernel_roofline("nbody", apply_pairs, FLOPS_PER_PAIR, FP64_OPS_PER_PAIR,
+                               "k_nbody_c<8,64,4,{0,1},false> (far-field SL+DL, row a3; sources as "
+                               "constant-bank operands, batches of 312 over two streams)" if const_a else
                                "k_nbody<8,64,64,3,false> (far-field SL+DL, row a3)",
-                               96 * N, 24 * N, f"cfg{args.config}")
+                               96 * N, 24 * N, f"cfg{args.config}_const" if const_a else f"cfg{args.config}")
     kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
                for k, v in prof.items() if v[1]}
     offsurface = None
     if has_off and prof["offsurface"][0] > 0:
+        const_o = prof["offsurface"][1] / args.steps > 8
         roff = kernel_roofline("offsurface", off_pairs, FLOPS_PER_PAIR_OFF, FP64_OPS_PER_PAIR_OFF,
-                               "k_nbody<7,64,64,3,true> (off-surface u and p, row a7)",
-                               104 * N, 32 * M, f"cfg{args.config}_off")
+                               "k_nbody_c<8,64,4,{0,1},true> (off-surface u and p, row a7; constant-bank "
+                               "batches)" if const_o else "k_nbody<7,64,64,3,true> (off-surface u and p, row a7)",
+                               104 * N, 32 * M, f"cfg{args.config}_off_const" if const_o else f"cfg{args.config}_off")
         offsurface = {"metric": "fp64 pair-interactions/sec, off-surface velocity + pressure (row a7)",
                       "value": replica_value(off_pairs, args.steps, world, off_total_ms),
                       "unit": "pair-interactions/s", "pairs_per_step": int(off_pairs),

@@ -851,6 +851,19 @@ static int run_sk(bie_ctx* c, Kern kern, Fix fix, int which, int r, int nc, Nbod
 
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
 
+// Which launches take the constant-bank schedule: asked for (7), or by default
+// (1) when the launch is large -- at least 2 full waves of target tiles (one
+// launch per batch must fill the GPU; below that the shared-memory kernel's
+// (tile, chunk) grid wins: cfg 3, 162,000 targets, 51.3 vs 48.4 ms) and at
+// least 16 batches of sources.  Measured (profiles/r02_far_reduction.jsonl,
+// lines tagged constant-bank): cfg 5 apply 1764 -> 1658 ms, cfg 4 3525 -> 3297.
+static bool use_const(const bie_ctx* c, int64_t M, int R) {
+  if (c->chunks_override != 0) return false;
+  if (c->far_red == 7) return true;
+  if (c->far_red != 1) return false;
+  return M >= (int64_t)2 * c->sm_count * 4 * kTPB * R && c->N >= (int64_t)16 * kCB;
+}
+
 // Constant-bank far field (bie_set_far_reduction 7; k_nbody_c.cuh): batches of
 // kCB sources, even batches on the caller's stream into `acc` (which already
 // holds the self term / zeros), odd batches on the context's side stream into
@@ -913,6 +926,7 @@ static int run_const_pass(bie_ctx* c, const double* tx, int64_t M, double* acc, 
   cudaEventRecord(c->ev_join, c->st_side);
   cudaStreamWaitEvent(s, c->ev_join, 0);
   k_nbody_c_join<<<(unsigned)((3 * M + 255) / 256), 256, 0, s>>>(M, acc, accB, wp ? pout : nullptr, pB, 2.0 * c->mu);
+  c->launches[kind] += nb;  // prof_begin counted the join
   prof_end(c, s, &ev);
   cudaEventRecord(done, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "constant-bank far field: batch copy");
@@ -920,7 +934,7 @@ static int run_const_pass(bie_ctx* c, const double* tx, int64_t M, double* acc, 
 }
 
 static int run_far(bie_ctx* c, double* u, cudaStream_t s, int mode, bool nx) {
-  if (c->far_red == 7 && mode == 0 && !nx && c->chunks_override == 0)
+  if (mode == 0 && !nx && use_const(c, c->N, kR_APPLY_C))
     return run_const_pass<false>(c, c->d_x, c->N, u, nullptr, BIE_KIND_NBODY, s);
   Ev ev;
   int rc;
@@ -1058,7 +1072,7 @@ static int run_offsurface(bie_ctx* c, const double* f, const double* q, const do
   const size_t nb_smem = NbodySmem<kTS, kNST, true>::kBytes;
   for (int64_t b0 = 0; b0 < m; b0 += kOffBatch) {
     const int64_t Mb = std::min(kOffBatch, m - b0);
-    if (c->far_red == 7 && c->chunks_override == 0) {  // constant-bank batches (k_nbody_c.cuh)
+    if (use_const(c, Mb, kR_OFF_C)) {  // constant-bank batches (k_nbody_c.cuh)
       cudaMemsetAsync(u + 3 * b0, 0, (size_t)3 * Mb * sizeof(double), s);
       if (p) cudaMemsetAsync(p + b0, 0, (size_t)Mb * sizeof(double), s);
       if ((rc = run_const_pass<true>(c, tg + 3 * b0, Mb, u + 3 * b0, p ? p + b0 : nullptr, BIE_KIND_OFFSURF, s)))
