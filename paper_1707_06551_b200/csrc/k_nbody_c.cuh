@@ -37,6 +37,7 @@ struct NbodyCArgs {
   double* pacc;      // [M] pressure accumulator (OFF; may be nullptr)
   int64_t M;
   int64_t k0;        // global index of the batch's first source (masking)
+  int64_t tbase;     // global node index of target 0 of this launch (masking; apply only)
   int ks;            // sources in the batch (<= kCB)
   int nsn;           // nodes per sphere (masking; apply only)
 };
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(TPB, 1) k_nbody_c(const NbodyCArgs A) {
   bool masked = false;
   if (!OFF) {  // does the batch [k0, k0 + ks) meet the spheres of this CTA's targets?
     const int64_t te = (tb + TPB * R < A.M ? tb + TPB * R : A.M) - 1;
-    const int64_t span_lo = (tb / A.nsn) * A.nsn, span_hi = (te / A.nsn + 1) * A.nsn;
+    const int64_t span_lo = ((A.tbase + tb) / A.nsn) * A.nsn, span_hi = ((A.tbase + te) / A.nsn + 1) * A.nsn;
     masked = A.k0 < span_hi && A.k0 + ks > span_lo;
   }
   if (!masked) {
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(TPB, 1) k_nbody_c(const NbodyCArgs A) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int64_t t = t0 + r * TPB < A.M ? t0 + r * TPB : A.M - 1;
-      lo[r] = (int)((t / A.nsn) * A.nsn - A.k0);
+      lo[r] = (int)(((A.tbase + t) / A.nsn) * A.nsn - A.k0);
     }
 #pragma unroll 1
     for (int s = 0; s < ks; ++s) {

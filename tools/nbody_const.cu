@@ -46,11 +46,15 @@ __device__ __forceinline__ void pair_g(const double2 s0, const double2 s1, const
     const double dx = xt[r][0] - s0.x, dy = xt[r][1] - s0.y, dz = xt[r][2] - s1.x;
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     const double y = rsq(r2);
-    const double rf = fma(dz, s4.x, fma(dy, s3.y, dx * s3.x));
     const double rn = fma(dz, s2.y, fma(dy, s2.x, dx * s1.y));
     const double rq = fma(dz, s5.y, fma(dy, s5.x, dx * s4.y));
     const double y2 = y * y;
+#ifdef T2CHAIN  // rho.f' accumulated onto (rho.n)(rho.q') y^2: no DFMA with three register operands
+    const double t2 = fma(dz, s4.x, fma(dy, s3.y, fma(dx, s3.x, (rn * rq) * y2)));
+#else
+    const double rf = fma(dz, s4.x, fma(dy, s3.y, dx * s3.x));
     const double t2 = fma(rn * rq, y2, rf);
+#endif
     const double sp = t2 * y2;
     acc[r][0] = fma(y, fma(dx, sp, s3.x), acc[r][0]);
     acc[r][1] = fma(y, fma(dy, sp, s3.y), acc[r][1]);
