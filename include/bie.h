@@ -383,7 +383,10 @@ int bie_set_self_kernel(bie_ctx* ctx, int variant);
  *   5 and 6 never do.  The sources are cut
  *   into batches of 312 records that are copied device-to-device into one of
  *   two __constant__ buffers; one launch per batch adds the batch's
- *   contribution at every target to an accumulator.  The FP64 instructions
+ *   contribution at every target of a sub-range (<= 655,360 targets, so that
+ *   the accumulators stay in L2 between launches; environment variable
+ *   BIE_CONST_SUB, read by bie_create, overrides the size, 0 = one range) to
+ *   an accumulator.  The FP64 instructions
  *   then take the source operands from the uniform datapath instead of the
  *   vector register file, which lifts the register-file read limit of the
  *   shared-memory kernel.  Even batches run on the caller's

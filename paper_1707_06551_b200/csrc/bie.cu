@@ -88,7 +88,7 @@ struct bie_ctx {
   double* d_part = nullptr;
   size_t part_cap = 0;  // doubles
   cudaStream_t st_side = nullptr;              // constant-bank far field: stream of the odd batches
-  int64_t const_sub = 0;                       // targets per sub-range of a constant-bank pass (0: all)
+  int64_t const_sub = 655360;                  // targets per sub-range of a constant-bank pass (0: all)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* d_sht = nullptr;  // fragment-order transform tables of k_sht
   int sht_occ = 1;          // resident k_sht CTAs per SM

@@ -10,7 +10,7 @@
 // DADD/DMUL/DFMA take them as UR operands, which cost no vector register-file
 // read (tools/nbody_const.cu: 5.81e11 vs 5.45e11 pairs/s on the cfg 5 shape).
 //
-// Schedule (host side in bie.cu, run_far_const / run_off_const): the sources
+// Schedule (host side in bie.cu, run_const_pass): the sources
 // are cut into batches of kCB records; a batch is copied device-to-device
 // into one of two constant buffers (the 64 KB bank holds 2 x kCB x 104 B) and
 // ONE launch adds its contribution at every target to an accumulator
@@ -18,7 +18,10 @@
 // accumulator A on the caller's stream, odd batches buffer 1 / accumulator B
 // on a side stream, so the ragged last wave of one launch overlaps the other
 // stream's launch; a final pass adds B to A.  Deterministic: the batch ->
-// accumulator assignment and the order within each are fixed.
+// accumulator assignment and the order within each are fixed.  A pass walks
+// the targets in sub-ranges (<= 655,360 targets, each against every batch) so
+// that positions + both accumulators of a sub-range stay L2-resident between
+// launches (DRAM per launch 2.9 MB -> 45 KB at cfg 5).
 // Self-sphere exclusion (reading R8): per-pair select, only in CTAs whose
 // target spheres overlap the batch's source range.
 #pragma once
