@@ -462,14 +462,21 @@ def test_stream_k_small_and_ragged(bie, oracle_mod, ns, p):
     _assert_parity(pr.cpu().numpy(), pref, "sk off p")
 
 
-@pytest.mark.parametrize("ns,p", [(1, 3), (2, 1), (3, 4), (7, 6), (40, 5), (12, 8), (5, 12)])
-def test_constant_bank_far_field(bie, oracle_mod, ns, p):
+@pytest.mark.parametrize("ns,p,sub", [(1, 3, None), (2, 1, None), (3, 4, None), (7, 6, None), (40, 5, None),
+                                      (12, 8, None), (5, 12, None), (7, 6, 100), (40, 5, 700), (12, 8, 1000)])
+def test_constant_bank_far_field(bie, oracle_mod, ns, p, sub, monkeypatch):
     """bie_set_far_reduction(7): sources as constant-bank operands in batches of
     312 records over two streams (k_nbody_c.cuh).  Apply (self-sphere exclusion
     in batches that straddle spheres, one batch only, ragged last batch and
     target tile) and off-surface u / p against the oracle; deterministic; a
     second context used in between must not disturb the first (the constant
-    buffers are shared by the process)."""
+    buffers are shared by the process).  sub: BIE_CONST_SUB (read by bie_create)
+    forces several target sub-ranges per pass on these small cases -- the path
+    cfg 4 / 5 take by default -- with ranges that cut through spheres."""
+    if sub is not None:
+        monkeypatch.setenv("BIE_CONST_SUB", str(sub))
+    else:
+        monkeypatch.delenv("BIE_CONST_SUB", raising=False)
     c, a, f, q, mu = _random_case(1500 + ns + p, ns, p, True, 1.2)
     ctx = bie.bie_create(c, a, p, mu)
     ctx2 = bie.bie_create(c[:1] + 100.0, a[:1], p, mu)
