@@ -378,8 +378,8 @@ int bie_set_self_kernel(bie_ctx* ctx, int variant);
  *   distributed shared memory in fixed rank order; smaller launches use 1.
  * 7: constant-bank batches (SL+DL apply without near exclusion, off-surface
  *   u / p; other far-field operators keep schedule 1).  Schedule 1 (the
- *   default) takes this path by itself for large launches (>= 2 waves of
- *   512-target tiles, i.e. >= 606,208 targets on 148 SMs, and >= 4992 sources);
+ *   default) takes this path by itself for large launches (>= 0.8 waves of
+ *   512-target tiles, i.e. >= 242,483 targets on 148 SMs, and >= 4992 sources);
  *   5 and 6 never do.  The sources are cut
  *   into batches of 312 records that are copied device-to-device into one of
  *   two __constant__ buffers; one launch per batch adds the batch's

@@ -854,16 +854,18 @@ static int run_sk(bie_ctx* c, Kern kern, Fix fix, int which, int r, int nc, Nbod
 // row a3: far-field smooth sum over all other spheres, accumulated onto u
 
 // Which launches take the constant-bank schedule: asked for (7), or by default
-// (1) when the launch is large -- at least 2 full waves of target tiles (one
-// launch per batch must fill the GPU; below that the shared-memory kernel's
-// (tile, chunk) grid wins: cfg 3, 162,000 targets, 51.3 vs 48.4 ms) and at
-// least 16 batches of sources.  Measured (profiles/r02_far_reduction.jsonl,
-// lines tagged constant-bank): cfg 5 apply 1764 -> 1658 ms, cfg 4 3525 -> 3297.
+// (1) when one launch (all targets x one batch) nearly fills the GPU -- at
+// least 0.8 waves of target tiles (242,483 targets on 148 SMs; the two streams
+// keep two launches in flight) -- and there are at least 16 batches of
+// sources.  Measured on lattices of unit spheres, p = 6 (tools/const_threshold.py,
+// profiles/r02_const_threshold.jsonl), k_nbody / k_nbody_c time: 98,000 nodes
+// 0.73, 196,000 1.01, 294,000 1.056, 392,000 1.052, 607,600 1.057, 980,000
+// 1.054; cfg 3 (162,000 nodes) 0.94.
 static bool use_const(const bie_ctx* c, int64_t M, int R) {
   if (c->chunks_override != 0) return false;
   if (c->far_red == 7) return true;
   if (c->far_red != 1) return false;
-  return M >= (int64_t)2 * c->sm_count * 4 * kTPB * R && c->N >= (int64_t)16 * kCB;
+  return 5 * M >= (int64_t)4 * c->sm_count * 4 * kTPB * R && c->N >= (int64_t)16 * kCB;
 }
 
 // Constant-bank far field (bie_set_far_reduction 7; k_nbody_c.cuh): batches of

@@ -422,11 +422,10 @@ def test_far_schedules_agree(bie, oracle_mod):
         out[mode] = res
     ctx.close()
     # 5 (always chained) and 6 (HBM partials + k_reduce): same sums, bit for bit; the
-    # default (1) takes the constant-bank batches for the apply at this size (same as
-    # 7; the 600,000 off-surface targets are below its threshold) and the chained
-    # schedule for K
+    # default (1) takes the constant-bank batches for the apply and the off-surface
+    # sums at this size (same as 7) and the chained schedule for K
     assert all(np.array_equal(a + 0.0, b + 0.0) for a, b in zip(out[5], out[6])), "chained"
-    assert np.array_equal(out[1][0], out[7][0]), "default != constant-bank apply at cfg 5"
+    assert all(np.array_equal(a, b) for a, b in zip(out[1][:3], out[7][:3])), "default != constant-bank at cfg 5"
     assert np.array_equal(out[1][3] + 0.0, out[5][3] + 0.0), "K: default != chained"
     for m in (1, 2, 7):  # 7: constant-bank batches (apply and off-surface; K keeps the default)
         for a, b, what in zip(out[0], out[m], ("apply", "offsurface u", "offsurface p", "K")):
