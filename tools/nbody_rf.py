@@ -15,6 +15,8 @@ INST = {
     "apply": "k_nbody<8, 64, 64, 3, false, 1, 2>",
     "off": "k_nbody<7, 64, 64, 3, true, 1, 2>",
     "K": "k_nbody<7, 64, 64, 3, false, 1, 2, 1>",
+    "apply_const": "k_nbody_c<8, 64, 4, 0, false>",   # sources as constant-bank operands
+    "off_const": "k_nbody_c<8, 64, 4, 0, true>",
 }
 
 
@@ -23,8 +25,9 @@ def main():
     if os.environ.get("NBODY_INST"):  # e.g. "k_nbody<4, 64, 64, 3, false, 1, 4>;k_nbody<...>"
         INST.clear()
         INST.update({str(i): v for i, v in enumerate(os.environ["NBODY_INST"].split(";"))})
-    src = '#include "k_nbody.cuh"\nnamespace bie {\n' + "".join(
-        f"template __global__ void {v}(const NbodyArgs);\n" for v in INST.values()) + "}\n"
+    src = '#include "k_nbody.cuh"\n#include "k_nbody_c.cuh"\nnamespace bie {\n' + "".join(
+        f"template __global__ void {v}(const {'NbodyCArgs' if v.startswith('k_nbody_c') else 'NbodyArgs'});\n"
+        for v in INST.values()) + "}\n"
     with tempfile.TemporaryDirectory() as td:
         cu = os.path.join(td, "k.cu")
         open(cu, "w").write(src)
