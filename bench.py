@@ -320,7 +320,7 @@ def run_gpu(args):
     if has_off and prof["offsurface"][0] > 0:
         const_o = prof["offsurface"][1] / args.steps > 8
         roff = kernel_roofline("offsurface", off_pairs, FLOPS_PER_PAIR_OFF, FP64_OPS_PER_PAIR_OFF,
-                               "k_nbody_c<8,64,4,{0,1},true> (off-surface u and p, row a7; constant-bank "
+                               "k_nbody_c<8,64,2,{0,1},true> (off-surface u and p, row a7; constant-bank "
                                "batches)" if const_o else "k_nbody<7,64,64,3,true> (off-surface u and p, row a7)",
                                104 * N, 32 * M, f"cfg{args.config}_off_const" if const_o else f"cfg{args.config}_off")
         offsurface = {"metric": "fp64 pair-interactions/sec, off-surface velocity + pressure (row a7)",

@@ -41,6 +41,10 @@ namespace {
 constexpr int kTPB = 64, kTS = 64, kNST = 3;
 constexpr int kR_APPLY = 8, kR_OFF = 7, kR_K = 7, kR_OFFK = 7;
 constexpr int kR_APPLY_C = 8, kR_OFF_C = 8, kUNR_C = 4;  // constant-bank kernels (k_nbody_c.cuh)
+#ifndef BIE_UNR_OFF_C
+#define BIE_UNR_OFF_C 2
+#endif
+constexpr int kUNR_OFF_C = BIE_UNR_OFF_C;  // off-surface batch-loop unroll (2 measured: see DESIGN.md 5.2)
 constexpr int64_t kOffBatch = 1 << 21;  // off-surface targets per batch (bounds scratch)
 constexpr double kScratchBytes = 3.0e9;  // cap on chunk-partial scratch
 
@@ -937,8 +941,9 @@ static int run_const_pass(bie_ctx* c, const double* tx, int64_t M, double* acc, 
         e = cudaMemcpyToSymbolAsync(c_nb_qn, c->d_qn3 + A.k0, (size_t)A.ks * sizeof(double),
                                     (size_t)w * kCB * sizeof(double), cudaMemcpyDeviceToDevice, sb);
       if (e != cudaSuccess) break;
-      if (w) k_nbody_c<R, kTPB, kUNR_C, 1, OFF><<<grid, kTPB, 0, sb>>>(A);
-      else k_nbody_c<R, kTPB, kUNR_C, 0, OFF><<<grid, kTPB, 0, sb>>>(A);
+      constexpr int UNR = OFF ? kUNR_OFF_C : kUNR_C;
+      if (w) k_nbody_c<R, kTPB, UNR, 1, OFF><<<grid, kTPB, 0, sb>>>(A);
+      else k_nbody_c<R, kTPB, UNR, 0, OFF><<<grid, kTPB, 0, sb>>>(A);
     }
     cudaEventRecord(c->ev_join, c->st_side);
     cudaStreamWaitEvent(s, c->ev_join, 0);

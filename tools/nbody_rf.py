@@ -16,7 +16,7 @@ INST = {
     "off": "k_nbody<7, 64, 64, 3, true, 1, 2>",
     "K": "k_nbody<7, 64, 64, 3, false, 1, 2, 1>",
     "apply_const": "k_nbody_c<8, 64, 4, 0, false>",   # sources as constant-bank operands
-    "off_const": "k_nbody_c<8, 64, 4, 0, true>",
+    "off_const": "k_nbody_c<8, 64, 2, 0, true>",
 }
 
 
